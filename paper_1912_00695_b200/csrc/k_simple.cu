@@ -1,0 +1,168 @@
+// One-thread-per-point stencil kernels (all three forms) and the small auxiliary kernels.
+//
+// The plain forms (basic DSE) are arithmetic-bound by design (3*SO+3 IEEE divisions per
+// point, the paper's OI comparison, BASELINE config 3); the factorised "simple" variant is
+// the kernel-choice baseline for the TMA 2.5D kernel in k_tma.cu.
+#include <cuda_runtime.h>
+
+#include "k_common.cuh"
+#include "kernels.h"
+
+namespace swb {
+
+template <int H, int FORM>
+__global__ void __launch_bounds__(128) k_simple(Geo g, Coef K, Ctl c, Peer p) {
+    const int z = g.z0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = g.y0 + blockIdx.y;
+    const int x = g.x0 + blockIdx.z;
+    const int lt = c.step % 3, ln = (c.step + 1) % 3, lp = (c.step + 2) % 3;
+    const float* __restrict__ ut = pick3(g.lev[0], g.lev[1], g.lev[2], lt);
+    const float* __restrict__ um = pick3(g.lev[0], g.lev[1], g.lev[2], lp);
+    float* __restrict__ un = pick3(g.lev[0], g.lev[1], g.lev[2], ln);
+    unsigned mine = 0u;
+    if (z < g.z1) {
+        const long long s0 = g.plane, s1 = g.P2;
+        const long long i = x * s0 + y * s1 + z;
+        const float u0 = ut[i], up = um[i], m = g.m[i], dmp = g.damp[i];
+        float v;
+        if constexpr (FORM == 1) {
+            v = plain_f64_point<H>(ut, i, s0, s1, u0, up, m, dmp, K);
+        } else if constexpr (FORM == 2) {
+            v = plain_f32_point<H>(ut, i, s0, s1, u0, up, m, dmp, K);
+        } else {
+            const float sx = lap_axis<H>(K, u0, [&](int k) { return ut[i + k * s0]; });
+            const float sy = lap_axis<H>(K, u0, [&](int k) { return ut[i + k * s1]; });
+            const float sz = lap_axis<H>(K, u0, [&](int k) { return ut[i + k]; });
+            v = combine_f64(K, lap_total(K, sx, sy, sz, u0), u0, up, m, dmp);
+        }
+        if (c.has_src && x == c.src_x && y == c.src_y && z == c.src_z)
+            v = inject_source(v, c.wavelet[c.step], m, static_cast<double>(K.dt));
+        un[i] = v;
+        if (x >= p.lo_first && x < p.lo_last)
+            pick3(p.lo_lev[0], p.lo_lev[1], p.lo_lev[2], ln)[(x + p.lo_shift) * s0 + y * s1 + z] = v;
+        if (x >= p.hi_first && x < p.hi_last)
+            pick3(p.hi_lev[0], p.hi_lev[1], p.hi_lev[2], ln)[(x + p.hi_shift) * s0 + y * s1 + z] = v;
+        mine = abs_bits(v);
+    }
+    block_max_commit(mine, c.smax + c.slot);
+}
+
+template <int H>
+static cudaError_t launch_simple_h(int form, const Geo& g, const Coef& K, const Ctl& c,
+                                   const Peer& p, cudaStream_t s) {
+    dim3 block(128);
+    dim3 grid(ceil_div(g.z1 - g.z0, 128), g.y1 - g.y0, g.x1 - g.x0);
+    if (grid.z == 0 || grid.y == 0) return cudaSuccess;
+    switch (form) {
+        case 1: k_simple<H, 1><<<grid, block, 0, s>>>(g, K, c, p); break;
+        case 2: k_simple<H, 2><<<grid, block, 0, s>>>(g, K, c, p); break;
+        default: k_simple<H, 0><<<grid, block, 0, s>>>(g, K, c, p); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ctl& c,
+                          const Peer& p, cudaStream_t s) {
+    switch (H) {
+        case 1: return launch_simple_h<1>(form, g, K, c, p, s);
+        case 2: return launch_simple_h<2>(form, g, K, c, p, s);
+        case 3: return launch_simple_h<3>(form, g, K, c, p, s);
+        case 4: return launch_simple_h<4>(form, g, K, c, p, s);
+        case 5: return launch_simple_h<5>(form, g, K, c, p, s);
+        case 6: return launch_simple_h<6>(form, g, K, c, p, s);
+        case 7: return launch_simple_h<7>(form, g, K, c, p, s);
+        case 8: return launch_simple_h<8>(form, g, K, c, p, s);
+        case 9: return launch_simple_h<9>(form, g, K, c, p, s);
+        case 10: return launch_simple_h<10>(form, g, K, c, p, s);
+        case 11: return launch_simple_h<11>(form, g, K, c, p, s);
+        case 12: return launch_simple_h<12>(form, g, K, c, p, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ---- auxiliary kernels ---------------------------------------------------------------
+
+// max|u| and non-finite detection over the cells of one level that the stencil never
+// writes (the ring of width H inside the grid plus, for a slab, nothing else): these stay
+// constant for the whole run, so the per-step whole-grid max of the reference
+// (src/executor.cpp:526-544) is max(ring_max[level], max over the updated points).
+__global__ void k_ring_max(const float* __restrict__ u, long long plane, int P2, int nx0, int nx1,
+                           int n1, int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
+                           int z_in1, unsigned* out) {
+    unsigned mine = 0u;
+    const long long total = static_cast<long long>(nx1 - nx0) * n1 * n2;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int z = static_cast<int>(t % n2);
+        const int y = static_cast<int>((t / n2) % n1);
+        const int x = nx0 + static_cast<int>(t / (static_cast<long long>(n2) * n1));
+        const bool interior = x >= x_in0 && x < x_in1 && y >= y_in0 && y < y_in1 && z >= z_in0 &&
+                              z < z_in1;
+        if (!interior) mine = max(mine, abs_bits(u[x * plane + y * P2 + z]));
+    }
+    block_max_commit(mine, out);
+}
+
+// Receiver sampling: u of the newest level at on-grid points, after injection — what the
+// reference's on_step(step, u, newest) callback observes (src/executor.cpp:595-596).
+__global__ void k_receivers(const float* __restrict__ un, const long long* __restrict__ idx, int n,
+                            float* __restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) {
+        const long long j = idx[r];
+        out[r] = j >= 0 ? un[j] : 0.0f;
+    }
+}
+
+// Halo-exchange ordering: spin until every linked neighbour has completed at least
+// `need` steps (counters live in this handle's memory and are written by the neighbours).
+__global__ void k_wait_flags(const volatile unsigned long long* flags, int mask,
+                             unsigned long long need) {
+    if (threadIdx.x < 2 && ((mask >> threadIdx.x) & 1)) {
+        while (flags[threadIdx.x] < need) __nanosleep(64);
+    }
+    __syncthreads();
+    __threadfence_system();
+}
+
+// Publish "I completed `done` steps" into each neighbour's flag slot (after the stencil
+// kernel in stream order, so all peer stores of that step are complete and visible).
+__global__ void k_signal_flags(unsigned long long* lo_flag, unsigned long long* hi_flag,
+                               unsigned long long done) {
+    __threadfence_system();
+    if (threadIdx.x == 0) {
+        if (lo_flag) atomicExch(lo_flag, done);
+        if (hi_flag) atomicExch(hi_flag, done);
+    }
+    __threadfence_system();
+}
+
+cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
+                            int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
+                            int z_in1, unsigned* out, cudaStream_t s) {
+    if (nx1 <= nx0) return cudaSuccess;
+    k_ring_max<<<592, 256, 0, s>>>(u, plane, P2, nx0, nx1, n1, n2, x_in0, x_in1, y_in0, y_in1,
+                                   z_in0, z_in1, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_receivers(const float* un, const long long* idx, int n, float* out,
+                             cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_receivers<<<ceil_div(n, 128), 128, 0, s>>>(un, idx, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const unsigned long long* flags, int mask,
+                              unsigned long long need, cudaStream_t s) {
+    k_wait_flags<<<1, 32, 0, s>>>(flags, mask, need);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_signal_flags(unsigned long long* lo_flag, unsigned long long* hi_flag,
+                                unsigned long long done, cudaStream_t s) {
+    k_signal_flags<<<1, 32, 0, s>>>(lo_flag, hi_flag, done);
+    return cudaGetLastError();
+}
+
+}  // namespace swb

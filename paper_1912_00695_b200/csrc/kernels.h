@@ -1,0 +1,44 @@
+// Kernel launchers (host-callable) implemented in k_simple.cu and k_tma.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "swb_internal.h"
+
+namespace swb {
+
+// One-thread-per-point stencil step; form: 0 factorised, 1 plain FP64, 2 plain FP32.
+cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ctl& c,
+                          const Peer& p, cudaStream_t s);
+
+// TMA 2.5D factorised stencil (k_tma.cu).  `plan` is produced by tma_plan().
+struct TmaPlan {
+    int ok;
+    int H;
+    int T1, T2;           // output tile rows (dim 1) and cols (dim 2)
+    int A;                // dim-2 halo rounded up to a multiple of 4
+    int stages;           // u-plane ring depth
+    int threads;
+    int smem_bytes;
+    int tiles_y, tiles_z, columns;  // column tiles
+    int zs;               // first (aligned) dim-2 column of tile 0
+    int grid;             // persistent CTAs
+    long long work;       // column tiles x planes
+    int variant;
+};
+TmaPlan tma_plan(int H, const Geo& g, int num_sms);
+// Encodes the tensor maps for the three u levels (once per handle).
+cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*3 x 128 B*/);
+cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
+                       const Ctl& c, const Peer& p, cudaStream_t s);
+
+cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
+                            int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
+                            int z_in1, unsigned* out, cudaStream_t s);
+cudaError_t launch_receivers(const float* un, const long long* idx, int n, float* out,
+                             cudaStream_t s);
+cudaError_t launch_wait_flags(const unsigned long long* flags, int mask,
+                              unsigned long long need, cudaStream_t s);
+cudaError_t launch_signal_flags(unsigned long long* lo_flag, unsigned long long* hi_flag,
+                                unsigned long long done, cudaStream_t s);
+
+}  // namespace swb

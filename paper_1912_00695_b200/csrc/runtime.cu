@@ -1,0 +1,649 @@
+// The C-ABI runtime (include/swb.h): device memory, streams, the time loop, halo linking.
+// It replaces the reference Engine (src/executor.cpp:140-606) for the acoustic IET.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/swb.h"
+#include "kernels.h"
+#include "swb_internal.h"
+
+using namespace swb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define SWB_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(SWB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+constexpr uint32_t kBlobMagic = 0x53574231u;  // "SWB1"
+
+struct IpcBlob {
+    uint32_t magic;
+    int32_t xg_off, nl0, n1, n2, P2, H;
+    int64_t level_floats;
+    cudaIpcMemHandle_t u_handle;
+    cudaIpcMemHandle_t flag_handle;
+};
+
+}  // namespace
+
+struct swb_handle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int n0 = 0, n1 = 0, n2 = 0, so = 0, H = 0, HU = 0, P2 = 0;
+    int lo = 0, hi = 0, gb = 0, ga = 0, nl0 = 0, xg_off = 0;
+    long long plane = 0, level_floats = 0;
+    int form = 0, time_block = 1;
+    float* u = nullptr;
+    float* m = nullptr;
+    float* damp = nullptr;
+    float* d_wavelet = nullptr;
+    int wavelet_len = 0;
+    unsigned* d_smax = nullptr;
+    int smax_cap = 0;
+    unsigned* d_ring = nullptr;  // [3]
+    bool ring_dirty = true;
+    // receivers
+    int n_rec = 0;
+    std::vector<int> rec_owned;          // global receiver index per owned receiver
+    long long* d_rec_idx = nullptr;      // local flat index per owned receiver
+    float* d_traces = nullptr;
+    int traces_cap = 0;
+    // stencil
+    Geo geo{};
+    Coef K{};
+    Ctl ctl{};
+    Peer peer{};
+    TmaPlan plan{};
+    alignas(128) unsigned char maps[3 * 128];
+    bool use_tma = false;
+    // halo links
+    unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
+    unsigned long long* lo_remote = nullptr; // lower neighbour's d_flags[1]
+    unsigned long long* hi_remote = nullptr; // upper neighbour's d_flags[0]
+    void* ipc_lo_u = nullptr;
+    void* ipc_hi_u = nullptr;
+    void* ipc_lo_f = nullptr;
+    void* ipc_hi_f = nullptr;
+    unsigned long long steps_done = 0;
+    // pending apply
+    int pend_step0 = 0, pend_nt = 0;
+    bool pending = false;
+    swb_stats stats{};
+    uint64_t launches = 0;
+};
+
+namespace {
+
+int setup_device(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(SWB_ECUDA, std::string("no CUDA device available (") +
+                                   cudaGetErrorString(e) + "); there is no CPU fallback");
+    if (device < 0 || device >= count) return fail(SWB_EINVAL, "device ordinal out of range");
+    cudaDeviceProp prop{};
+    SWB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(SWB_ECUDA, std::string("device ") + prop.name + " is sm_" +
+                                   std::to_string(prop.major * 10 + prop.minor) +
+                                   "; this library is built for sm_100a (B200) only");
+    SWB_CUDA(cudaSetDevice(device));
+    return SWB_OK;
+}
+
+void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
+    std::memset(&K, 0, sizeof K);
+    for (int k = 0; k <= H; ++k) K.c[k] = w[H + k];
+    const double c0 = K.c[0], c1 = K.c[1];
+    K.R_d = c0 + 2.0 * c1;
+    K.R = static_cast<float>(K.R_d);
+    for (int d = 0; d < 3; ++d) {
+        K.h[d] = p->spacing[d];
+        const double hd = static_cast<double>(p->spacing[d]);
+        K.inv_h2[d] = 1.0 / (hd * hd);
+    }
+    K.dt = p->dt;
+    const double dt = static_cast<double>(p->dt);
+    K.inv_dt2 = 1.0 / (dt * dt);
+    K.half_inv_dt = 0.5 / dt;
+    K.inject = dt * dt;
+    K.iso = (p->spacing[0] == p->spacing[1] && p->spacing[1] == p->spacing[2]) ? 1 : 0;
+}
+
+int ensure_smax(swb_handle* h, int nt) {
+    if (nt <= h->smax_cap) return SWB_OK;
+    if (h->d_smax) cudaFree(h->d_smax);
+    h->d_smax = nullptr;
+    int cap = std::max(nt, 1024);
+    SWB_CUDA(cudaMalloc(&h->d_smax, sizeof(unsigned) * cap));
+    h->smax_cap = cap;
+    return SWB_OK;
+}
+
+int ensure_traces(swb_handle* h, int nt) {
+    const int owned = static_cast<int>(h->rec_owned.size());
+    if (owned == 0) return SWB_OK;
+    long long need = static_cast<long long>(nt) * owned;
+    if (need <= h->traces_cap) return SWB_OK;
+    if (h->d_traces) cudaFree(h->d_traces);
+    h->d_traces = nullptr;
+    SWB_CUDA(cudaMalloc(&h->d_traces, sizeof(float) * need));
+    h->traces_cap = static_cast<int>(need);
+    return SWB_OK;
+}
+
+int refresh_ring(swb_handle* h) {
+    if (!h->ring_dirty) return SWB_OK;
+    SWB_CUDA(cudaMemsetAsync(h->d_ring, 0, 3 * sizeof(unsigned), h->stream));
+    // owned planes [gb, gb + hi - lo); interior = updated region
+    const int own0 = h->gb, own1 = h->gb + (h->hi - h->lo);
+    for (int l = 0; l < 3; ++l) {
+        SWB_CUDA(launch_ring_max(h->u + l * h->level_floats, h->plane, h->P2, own0, own1, h->n1,
+                                 h->n2, h->geo.x0, h->geo.x1, h->geo.y0, h->geo.y1, h->geo.z0,
+                                 h->geo.z1, h->d_ring + l, h->stream));
+    }
+    h->ring_dirty = false;
+    return SWB_OK;
+}
+
+int enqueue_steps(swb_handle* h, int step0, int nt) {
+    for (int i = 0; i < nt; ++i) {
+        const int s = step0 + i;
+        const bool linked = h->lo_remote || h->hi_remote;
+        if (linked) {
+            const int mask = (h->lo_remote ? 1 : 0) | (h->hi_remote ? 2 : 0);
+            SWB_CUDA(launch_wait_flags(h->d_flags, mask, h->steps_done + i, h->stream));
+            ++h->launches;
+        }
+        Ctl c = h->ctl;
+        c.step = s;
+        c.slot = i;
+        if (h->use_tma) {
+            SWB_CUDA(launch_tma(h->plan, h->maps, h->geo, h->K, c, h->peer, h->stream));
+        } else {
+            const int form = h->form == SWB_FORM_PLAIN_F64 ? 1 : h->form == SWB_FORM_PLAIN_F32 ? 2 : 0;
+            SWB_CUDA(launch_simple(h->H, form, h->geo, h->K, c, h->peer, h->stream));
+        }
+        ++h->launches;
+        if (!h->rec_owned.empty()) {
+            const int owned = static_cast<int>(h->rec_owned.size());
+            SWB_CUDA(launch_receivers(h->u + ((s + 1) % 3) * h->level_floats, h->d_rec_idx, owned,
+                                      h->d_traces + static_cast<long long>(i) * owned, h->stream));
+            ++h->launches;
+        }
+        if (linked) {
+            SWB_CUDA(launch_signal_flags(h->lo_remote, h->hi_remote, h->steps_done + i + 1,
+                                         h->stream));
+            ++h->launches;
+        }
+    }
+    h->steps_done += nt;
+    return SWB_OK;
+}
+
+void compute_peer_ranges(swb_handle* h) {
+    // planes mirrored to the lower neighbour: global [lo, lo+HU) ∩ updated; upper: [hi-HU, hi) ∩ updated
+    Peer& p = h->peer;
+    const int upd0 = h->geo.x0, upd1 = h->geo.x1;  // local
+    if (p.lo_lev[0]) {
+        p.lo_first = std::max(upd0, h->gb);
+        p.lo_last = std::min(upd1, h->gb + h->HU);
+    } else {
+        p.lo_first = p.lo_last = 0;
+    }
+    if (p.hi_lev[0]) {
+        const int own1 = h->gb + (h->hi - h->lo);
+        p.hi_first = std::max(upd0, own1 - h->HU);
+        p.hi_last = std::min(upd1, own1);
+    } else {
+        p.hi_first = p.hi_last = 0;
+    }
+    if (p.lo_first >= p.lo_last) p.lo_first = p.lo_last = 0;
+    if (p.hi_first >= p.hi_last) p.hi_first = p.hi_last = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* swb_last_error(void) { return g_err.c_str(); }
+
+const char* swb_version(void) {
+    return "swb 0.1 (sm_100a; kernels: factorised TMA 2.5D, factorised simple, plain f64, plain f32)";
+}
+
+int swb_create(const swb_problem* p, swb_handle** out) {
+    if (!p || !out) return fail(SWB_EINVAL, "null argument");
+    *out = nullptr;
+    for (int d = 0; d < 3; ++d) {
+        if (p->shape[d] < 1) return fail(SWB_EINVAL, "grid shape must be positive");
+        if (!(p->spacing[d] > 0.0f)) return fail(SWB_EINVAL, "grid spacing must be positive");
+    }
+    if (p->space_order < 2 || p->space_order % 2 != 0)
+        return fail(SWB_EINVAL, "space_order must be an even integer >= 2");
+    if (p->space_order > 2 * kMaxH)
+        return fail(SWB_EINVAL, "space_order above 24 is not supported");
+    if (!(p->dt > 0.0f)) return fail(SWB_EINVAL, "dt must be positive");
+    if (!p->m) return fail(SWB_EINVAL, "m (squared slowness) is required");
+    if (p->form < 0 || p->form > 3) return fail(SWB_EINVAL, "unknown stencil form");
+    if (p->time_block < 0) return fail(SWB_EINVAL, "time_block must be >= 1");
+    const int HU = p->space_order / 2;
+    const int H = std::max(HU, 1);  // widest halo among u (SO/2), m and damp (1): src/pipeline.cpp:79-88
+    const char* dn[3] = {"x", "y", "z"};
+    for (int d = 0; d < 3; ++d)
+        if (p->shape[d] - 1 - H < H)
+            return fail(SWB_EINVAL, "grid extent " + std::to_string(p->shape[d]) + " in " + dn[d] +
+                                        " is too small for halo " + std::to_string(H));
+    int lo = 0, hi = p->shape[0];
+    if (p->slab_hi > 0) {
+        lo = p->slab_lo;
+        hi = p->slab_hi;
+        if (lo < 0 || hi > p->shape[0] || lo >= hi) return fail(SWB_EINVAL, "bad slab range");
+        if (hi - lo < HU) return fail(SWB_EINVAL, "slab thinner than SO/2 planes");
+    }
+    if (p->has_source) {
+        for (int d = 0; d < 3; ++d)
+            if (p->source[d] < HU || p->source[d] > p->shape[d] - 1 - HU)
+                return fail(SWB_EINVAL, "source point must lie in the updatable interior");
+        if (!p->wavelet || p->wavelet_len < 1)
+            return fail(SWB_EINVAL, "source wavelet missing");
+    }
+    if (p->n_receivers < 0 || (p->n_receivers > 0 && !p->receivers))
+        return fail(SWB_EINVAL, "bad receiver list");
+    for (int r = 0; r < p->n_receivers; ++r)
+        for (int d = 0; d < 3; ++d)
+            if (p->receivers[3 * r + d] < 0 || p->receivers[3 * r + d] >= p->shape[d])
+                return fail(SWB_EINVAL, "receiver " + std::to_string(r) + " lies outside the grid");
+    int rc = setup_device(p->device);
+    if (rc) return rc;
+
+    auto* h = new swb_handle();
+    h->device = p->device;
+    h->n0 = p->shape[0];
+    h->n1 = p->shape[1];
+    h->n2 = p->shape[2];
+    h->so = p->space_order;
+    h->HU = HU;
+    h->H = H;
+    h->P2 = (h->n2 + 31) / 32 * 32;
+    h->lo = lo;
+    h->hi = hi;
+    h->gb = lo > 0 ? HU : 0;
+    h->ga = hi < h->n0 ? HU : 0;
+    h->nl0 = (hi - lo) + h->gb + h->ga;
+    h->xg_off = lo - h->gb;
+    h->plane = static_cast<long long>(h->n1) * h->P2;
+    h->level_floats = h->plane * h->nl0;
+    h->form = p->form;
+    h->time_block = std::max(1, p->time_block);
+
+    auto cleanup = [&](int code) {
+        swb_destroy(h);
+        return code;
+    };
+#define SWB_CUDA_C(call)                                                                   \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return cleanup(fail(SWB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+    } while (0)
+
+    SWB_CUDA_C(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    SWB_CUDA_C(cudaEventCreate(&h->ev0));
+    SWB_CUDA_C(cudaEventCreate(&h->ev1));
+    SWB_CUDA_C(cudaMalloc(&h->u, sizeof(float) * 3 * h->level_floats));
+    SWB_CUDA_C(cudaMalloc(&h->m, sizeof(float) * h->level_floats));
+    SWB_CUDA_C(cudaMalloc(&h->damp, sizeof(float) * h->level_floats));
+    SWB_CUDA_C(cudaMemsetAsync(h->u, 0, sizeof(float) * 3 * h->level_floats, h->stream));
+    SWB_CUDA_C(cudaMemsetAsync(h->m, 0, sizeof(float) * h->level_floats, h->stream));
+    SWB_CUDA_C(cudaMemsetAsync(h->damp, 0, sizeof(float) * h->level_floats, h->stream));
+    SWB_CUDA_C(cudaMalloc(&h->d_ring, 3 * sizeof(unsigned)));
+    SWB_CUDA_C(cudaMalloc(&h->d_flags, 2 * sizeof(unsigned long long)));
+    SWB_CUDA_C(cudaMemsetAsync(h->d_flags, 0, 2 * sizeof(unsigned long long), h->stream));
+
+    // m / damp for every local plane (ghost planes included; they are never read).
+    const size_t row = sizeof(float) * h->n2;
+    const float* m_src = p->m + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
+    SWB_CUDA_C(cudaMemcpy2DAsync(h->m, sizeof(float) * h->P2, m_src, row, row,
+                                 static_cast<size_t>(h->nl0) * h->n1, cudaMemcpyHostToDevice,
+                                 h->stream));
+    if (p->damp) {
+        const float* d_src = p->damp + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
+        SWB_CUDA_C(cudaMemcpy2DAsync(h->damp, sizeof(float) * h->P2, d_src, row, row,
+                                     static_cast<size_t>(h->nl0) * h->n1, cudaMemcpyHostToDevice,
+                                     h->stream));
+    }
+    // FD weights: float(c_k) as the interpreter rounds them (src/executor.cpp:136-138).
+    std::vector<float> w(static_cast<size_t>(2 * HU + 1));
+    if (p->weights) {
+        std::memcpy(w.data(), p->weights, sizeof(float) * w.size());
+    } else {
+        int64_t num[2 * kMaxH + 1], den[2 * kMaxH + 1];
+        swb_fd_weights(2, p->space_order, num, den);
+        for (size_t i = 0; i < w.size(); ++i)
+            w[i] = static_cast<float>(static_cast<double>(num[i]) / static_cast<double>(den[i]));
+    }
+    // With SO=2 the halo H (=1) equals HU; Coef carries c_0..c_HU.
+    coef_from(p, HU, w.data(), h->K);
+
+    // Geometry: update interior [H, n-H) in every dim, intersected with the owned slab.
+    Geo& g = h->geo;
+    for (int l = 0; l < 3; ++l) g.lev[l] = h->u + l * h->level_floats;
+    g.m = h->m;
+    g.damp = h->damp;
+    g.plane = h->plane;
+    g.P2 = h->P2;
+    g.n1 = h->n1;
+    g.n2 = h->n2;
+    g.x0 = std::max(lo, H) - h->xg_off;
+    g.x1 = std::min(hi, h->n0 - H) - h->xg_off;
+    if (g.x1 < g.x0) g.x1 = g.x0;
+    g.y0 = H;
+    g.y1 = h->n1 - H;
+    g.z0 = H;
+    g.z1 = h->n2 - H;
+    g.xg_off = h->xg_off;
+
+    // Source / wavelet / receivers
+    Ctl& c = h->ctl;
+    c.has_src = 0;
+    if (p->has_source) {
+        h->wavelet_len = p->wavelet_len;
+        SWB_CUDA_C(cudaMalloc(&h->d_wavelet, sizeof(float) * p->wavelet_len));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_wavelet, p->wavelet, sizeof(float) * p->wavelet_len,
+                                   cudaMemcpyHostToDevice, h->stream));
+        if (p->source[0] >= lo && p->source[0] < hi) {
+            c.has_src = 1;
+            c.src_x = p->source[0] - h->xg_off;
+            c.src_y = p->source[1];
+            c.src_z = p->source[2];
+        }
+    }
+    c.wavelet = h->d_wavelet;
+    c.wavelet_len = h->wavelet_len;
+    h->n_rec = p->n_receivers;
+    std::vector<long long> ridx;
+    for (int r = 0; r < p->n_receivers; ++r) {
+        const int* q = p->receivers + 3 * r;
+        if (q[0] >= lo && q[0] < hi) {
+            h->rec_owned.push_back(r);
+            ridx.push_back((q[0] - h->xg_off) * h->plane + static_cast<long long>(q[1]) * h->P2 + q[2]);
+        }
+    }
+    if (!ridx.empty()) {
+        SWB_CUDA_C(cudaMalloc(&h->d_rec_idx, sizeof(long long) * ridx.size()));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_idx, ridx.data(), sizeof(long long) * ridx.size(),
+                                   cudaMemcpyHostToDevice, h->stream));
+    }
+    // Kernel choice: the TMA 2.5D kernel for the factorised form when the plan fits.
+    if (h->form == SWB_FORM_FACTORISED) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+        h->plan = tma_plan(HU, g, sms);
+        if (h->plan.ok) {
+            SWB_CUDA_C(tma_make_maps(h->plan, g, h->nl0, h->maps));
+            h->use_tma = true;
+        }
+    }
+    h->stats.kernel_variant = h->use_tma ? h->plan.variant : 100 + h->form;
+    h->stats.launch_steps = 1;
+    compute_peer_ranges(h);
+    SWB_CUDA_C(cudaStreamSynchronize(h->stream));
+    *out = h;
+#undef SWB_CUDA_C
+    return SWB_OK;
+}
+
+int swb_set_level(swb_handle* h, int level, const float* src) {
+    if (!h || !src || level < 0 || level > 2) return fail(SWB_EINVAL, "bad set_level arguments");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is pending");
+    SWB_CUDA(cudaSetDevice(h->device));
+    const size_t row = sizeof(float) * h->n2;
+    const float* s = src + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
+    SWB_CUDA(cudaMemcpy2DAsync(h->u + level * h->level_floats, sizeof(float) * h->P2, s, row, row,
+                               static_cast<size_t>(h->nl0) * h->n1, cudaMemcpyHostToDevice,
+                               h->stream));
+    h->ring_dirty = true;
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    return SWB_OK;
+}
+
+int swb_get_level(swb_handle* h, int level, float* dst) {
+    if (!h || !dst || level < 0 || level > 2) return fail(SWB_EINVAL, "bad get_level arguments");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is pending");
+    SWB_CUDA(cudaSetDevice(h->device));
+    const size_t row = sizeof(float) * h->n2;
+    float* d = dst + static_cast<size_t>(h->lo) * h->n1 * h->n2;
+    SWB_CUDA(cudaMemcpy2DAsync(d, row, h->u + level * h->level_floats + h->gb * h->plane,
+                               sizeof(float) * h->P2, row,
+                               static_cast<size_t>(h->hi - h->lo) * h->n1, cudaMemcpyDeviceToHost,
+                               h->stream));
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    return SWB_OK;
+}
+
+int swb_apply_async(swb_handle* h, int step0, int nt) {
+    if (!h) return fail(SWB_EINVAL, "null handle");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is already pending");
+    if (step0 < 0 || nt < 0) return fail(SWB_EINVAL, "steps must be non-negative");
+    if (h->ctl.wavelet && step0 + nt > h->wavelet_len)
+        return fail(SWB_EINVAL, "source wavelet shorter than the number of steps");
+    SWB_CUDA(cudaSetDevice(h->device));
+    int rc = ensure_smax(h, nt);
+    if (rc) return rc;
+    rc = ensure_traces(h, nt);
+    if (rc) return rc;
+    rc = refresh_ring(h);
+    if (rc) return rc;
+    if (nt > 0) SWB_CUDA(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned) * nt, h->stream));
+    h->launches = 0;
+    h->ctl.smax = h->d_smax;
+    SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+    rc = enqueue_steps(h, step0, nt);
+    if (rc) return rc;
+    SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+    h->pend_step0 = step0;
+    h->pend_nt = nt;
+    h->pending = true;
+    return SWB_OK;
+}
+
+int swb_collect(swb_handle* h, float* step_max_abs, int32_t* first_bad_step, float* rec_traces) {
+    if (!h) return fail(SWB_EINVAL, "null handle");
+    if (!h->pending) return fail(SWB_EINVAL, "no apply pending");
+    SWB_CUDA(cudaSetDevice(h->device));
+    h->pending = false;
+    const int nt = h->pend_nt, step0 = h->pend_step0;
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    h->stats.device_ms = ms;
+    h->stats.kernel_launches = h->launches;
+    const uint64_t per_step =
+        static_cast<uint64_t>(std::max(0, h->geo.x1 - h->geo.x0)) *
+            static_cast<uint64_t>(h->geo.y1 - h->geo.y0) * static_cast<uint64_t>(h->geo.z1 - h->geo.z0) +
+        (h->ctl.has_src ? 1u : 0u);
+    h->stats.point_updates += per_step * static_cast<uint64_t>(nt);
+    std::vector<unsigned> smax(static_cast<size_t>(nt)), ring(3);
+    if (nt > 0)
+        SWB_CUDA(cudaMemcpy(smax.data(), h->d_smax, sizeof(unsigned) * nt, cudaMemcpyDeviceToHost));
+    SWB_CUDA(cudaMemcpy(ring.data(), h->d_ring, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost));
+    int bad = -1;
+    for (int i = 0; i < nt; ++i) {
+        const unsigned bits = std::max(smax[i], ring[(step0 + i + 1) % 3]);
+        float v;
+        if (bits >= 0x7f800000u) {
+            v = std::nanf("");
+            if (bad < 0) bad = step0 + i;
+        } else {
+            std::memcpy(&v, &bits, sizeof v);
+        }
+        if (step_max_abs) step_max_abs[i] = v;
+    }
+    if (first_bad_step) *first_bad_step = bad;
+    if (rec_traces && h->n_rec > 0) {
+        const int owned = static_cast<int>(h->rec_owned.size());
+        std::memset(rec_traces, 0, sizeof(float) * static_cast<size_t>(nt) * h->n_rec);
+        if (owned > 0 && nt > 0) {
+            std::vector<float> t(static_cast<size_t>(nt) * owned);
+            SWB_CUDA(cudaMemcpy(t.data(), h->d_traces, sizeof(float) * t.size(),
+                                cudaMemcpyDeviceToHost));
+            for (int i = 0; i < nt; ++i)
+                for (int r = 0; r < owned; ++r)
+                    rec_traces[static_cast<size_t>(i) * h->n_rec + h->rec_owned[r]] =
+                        t[static_cast<size_t>(i) * owned + r];
+        }
+    }
+    if (bad >= 0)
+        return fail(SWB_EUNSTABLE,
+                    "non-finite wave field at step " + std::to_string(bad) + " (unstable dt?)");
+    return SWB_OK;
+}
+
+int swb_apply(swb_handle* h, int step0, int nt, float* step_max_abs, int32_t* first_bad_step,
+              float* rec_traces) {
+    int rc = swb_apply_async(h, step0, nt);
+    if (rc) return rc;
+    return swb_collect(h, step_max_abs, first_bad_step, rec_traces);
+}
+
+void* swb_stream(swb_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int swb_get_stats(swb_handle* h, swb_stats* out) {
+    if (!h || !out) return fail(SWB_EINVAL, "null argument");
+    *out = h->stats;
+    return SWB_OK;
+}
+
+int swb_destroy(swb_handle* h) {
+    if (!h) return SWB_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->ipc_lo_u) cudaIpcCloseMemHandle(h->ipc_lo_u);
+    if (h->ipc_hi_u) cudaIpcCloseMemHandle(h->ipc_hi_u);
+    if (h->ipc_lo_f) cudaIpcCloseMemHandle(h->ipc_lo_f);
+    if (h->ipc_hi_f) cudaIpcCloseMemHandle(h->ipc_hi_f);
+    for (void* q : {static_cast<void*>(h->u), static_cast<void*>(h->m), static_cast<void*>(h->damp),
+                    static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
+                    static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
+                    static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags)})
+        if (q) cudaFree(q);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return SWB_OK;
+}
+
+// ---- halo linking ----------------------------------------------------------------------
+
+int swb_link_local(swb_handle* lower, swb_handle* upper) {
+    if (!lower || !upper) return fail(SWB_EINVAL, "null handle");
+    if (lower->hi != upper->lo || lower->n1 != upper->n1 || lower->n2 != upper->n2 ||
+        lower->HU != upper->HU)
+        return fail(SWB_EINVAL, "handles are not adjacent slabs of one grid");
+    if (lower->device != upper->device) {
+        int can = 0;
+        SWB_CUDA(cudaDeviceCanAccessPeer(&can, lower->device, upper->device));
+        if (!can) return fail(SWB_ECUDA, "no peer access between the two devices");
+        cudaSetDevice(lower->device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(upper->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(SWB_ECUDA, cudaGetErrorString(e));
+        cudaGetLastError();
+        cudaSetDevice(upper->device);
+        e = cudaDeviceEnablePeerAccess(lower->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(SWB_ECUDA, cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+    for (int l = 0; l < 3; ++l) {
+        lower->peer.hi_lev[l] = upper->u + l * upper->level_floats;
+        upper->peer.lo_lev[l] = lower->u + l * lower->level_floats;
+    }
+    lower->peer.hi_shift = lower->xg_off - upper->xg_off;
+    upper->peer.lo_shift = upper->xg_off - lower->xg_off;
+    lower->hi_remote = upper->d_flags + 0;
+    upper->lo_remote = lower->d_flags + 1;
+    compute_peer_ranges(lower);
+    compute_peer_ranges(upper);
+    return SWB_OK;
+}
+
+int swb_export_ghosts(swb_handle* h, void* blob, size_t* blob_len) {
+    if (!h || !blob_len) return fail(SWB_EINVAL, "null argument");
+    if (!blob || *blob_len < sizeof(IpcBlob)) {
+        *blob_len = sizeof(IpcBlob);
+        return blob ? fail(SWB_EINVAL, "blob buffer too small") : SWB_OK;
+    }
+    SWB_CUDA(cudaSetDevice(h->device));
+    IpcBlob b{};
+    b.magic = kBlobMagic;
+    b.xg_off = h->xg_off;
+    b.nl0 = h->nl0;
+    b.n1 = h->n1;
+    b.n2 = h->n2;
+    b.P2 = h->P2;
+    b.H = h->HU;
+    b.level_floats = h->level_floats;
+    SWB_CUDA(cudaIpcGetMemHandle(&b.u_handle, h->u));
+    SWB_CUDA(cudaIpcGetMemHandle(&b.flag_handle, h->d_flags));
+    std::memcpy(blob, &b, sizeof b);
+    *blob_len = sizeof b;
+    return SWB_OK;
+}
+
+int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
+                        const void* upper_blob, size_t upper_len) {
+    if (!h) return fail(SWB_EINVAL, "null handle");
+    SWB_CUDA(cudaSetDevice(h->device));
+    auto open = [&](const void* blob, size_t len, IpcBlob& b, void** u, void** f) -> int {
+        if (len < sizeof(IpcBlob)) return fail(SWB_EINVAL, "short neighbour blob");
+        std::memcpy(&b, blob, sizeof b);
+        if (b.magic != kBlobMagic || b.n1 != h->n1 || b.n2 != h->n2 || b.P2 != h->P2 || b.H != h->HU)
+            return fail(SWB_EINVAL, "neighbour blob does not describe a slab of this grid");
+        SWB_CUDA(cudaIpcOpenMemHandle(u, b.u_handle, cudaIpcMemLazyEnablePeerAccess));
+        SWB_CUDA(cudaIpcOpenMemHandle(f, b.flag_handle, cudaIpcMemLazyEnablePeerAccess));
+        return SWB_OK;
+    };
+    if (lower_blob && lower_len) {
+        IpcBlob b;
+        int rc = open(lower_blob, lower_len, b, &h->ipc_lo_u, &h->ipc_lo_f);
+        if (rc) return rc;
+        float* base = static_cast<float*>(h->ipc_lo_u);
+        for (int l = 0; l < 3; ++l) h->peer.lo_lev[l] = base + l * b.level_floats;
+        h->peer.lo_shift = h->xg_off - b.xg_off;
+        h->lo_remote = static_cast<unsigned long long*>(h->ipc_lo_f) + 1;
+    }
+    if (upper_blob && upper_len) {
+        IpcBlob b;
+        int rc = open(upper_blob, upper_len, b, &h->ipc_hi_u, &h->ipc_hi_f);
+        if (rc) return rc;
+        float* base = static_cast<float*>(h->ipc_hi_u);
+        for (int l = 0; l < 3; ++l) h->peer.hi_lev[l] = base + l * b.level_floats;
+        h->peer.hi_shift = h->xg_off - b.xg_off;
+        h->hi_remote = static_cast<unsigned long long*>(h->ipc_hi_f) + 0;
+    }
+    compute_peer_ranges(h);
+    return SWB_OK;
+}
+
+}  // extern "C"

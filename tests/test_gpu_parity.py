@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+* plain FP64 kernel (basic DSE): bit-exact with the reference interpreter;
+* factorised TMA kernel (aggressive DSE, sign-corrected): relative L2 <= 1e-5 in FP32
+  after nt steps, receiver traces to the same tolerance, source/receiver indexing exact;
+* plain FP32 kernel (the paper's OPS form): documented looser tolerance.
+The golden fixtures come from the reference's own exec::run (tests/golden/make_golden.py).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1912_00695_b200 as P
+from oracle import bindings as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+META = json.load(open(os.path.join(GOLD, "golden.json")))
+CASES = [k for k in META if k != "kat"]
+TOL = 1e-5          # north star: relative L2 <= 1e-5 in FP32 after nt steps
+TOL_F32_PLAIN = 2e-4  # paper-faithful FP32 term-by-term form (1.2e-5 .. 3e-4)
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def golden_problem(name):
+    m = META[name]
+    z = np.load(os.path.join(GOLD, name + ".npz"))
+    vel = z["velocity"] if "velocity" in z else None
+    cfg = P.WaveProblemConfig(shape=tuple(m["shape"]), spacing=(10.0, 10.0, 10.0),
+                              space_order=m["space_order"], steps=m["steps"], velocity_field=vel,
+                              damp_max=m["damp_max"], damp_width=m["damp_width"])
+    init = list(z["initial_u"]) if "initial_u" in z else None
+    return m, z, P.make_wave_problem(cfg), init
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_plain_f64_bit_exact_against_reference_goldens(name):
+    m, z, prob, init = golden_problem(name)
+    res = P.run(prob, P.RunOptions(initial_u=init), dse=P.DseLevel.basic, receivers=z["receivers"])
+    for l in range(3):
+        assert hashlib.sha256(res.u.data[l].tobytes()).hexdigest() == m["levels_sha256"][l], l
+    assert np.array_equal(res.step_max_abs, z["step_max_abs"])
+    assert np.array_equal(res.rec_traces, z["rec_traces"])
+    assert res.point_updates == m["point_updates"]
+    assert res.final_level == m["final_level"]
+
+
+@pytest.mark.parametrize("form", ["factorised", "factorised_simple"])
+@pytest.mark.parametrize("name", CASES)
+def test_factorised_within_tolerance_of_reference_goldens(name, form):
+    m, z, prob, init = golden_problem(name)
+    res = P.run(prob, P.RunOptions(initial_u=init), form=form, receivers=z["receivers"])
+    ref = O.port_run(O.OracleConfig(shape=prob.shape, space_order=prob.space_order, steps=prob.steps,
+                                    velocity_field=z["velocity"] if "velocity" in z else None,
+                                    damp_max=m["damp_max"], damp_width=m["damp_width"]),
+                     initial_u=init, receivers=z["receivers"])
+    for l in range(3):
+        assert hashlib.sha256(ref["levels"][l].tobytes()).hexdigest() == m["levels_sha256"][l]
+        assert rel_l2(res.u.data[l], ref["levels"][l]) <= TOL, l
+    assert rel_l2(res.step_max_abs, z["step_max_abs"]) <= TOL
+    assert rel_l2(res.rec_traces, z["rec_traces"]) <= TOL
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_plain_f32_within_documented_tolerance(name):
+    m, z, prob, init = golden_problem(name)
+    res = P.run(prob, P.RunOptions(initial_u=init), form="plain_f32", receivers=z["receivers"])
+    ref = O.port_run(O.OracleConfig(shape=prob.shape, space_order=prob.space_order, steps=prob.steps,
+                                    velocity_field=z["velocity"] if "velocity" in z else None,
+                                    damp_max=m["damp_max"], damp_width=m["damp_width"]),
+                     initial_u=init)
+    fl = res.final_level
+    assert rel_l2(res.u.data[fl], ref["levels"][fl]) <= TOL_F32_PLAIN
+
+
+@pytest.mark.parametrize("form", ["factorised", "plain_f64", "plain_f32", "factorised_simple"])
+def test_source_index_bit_exact(form):
+    """From a zero field with a non-zero first sample, step 0 writes exactly one non-zero
+    cell: the source point, with the reference's two-rounding injection value."""
+    shape, so = (20, 22, 24), 8
+    wav = np.zeros(4, np.float32)
+    wav[0] = 0.75
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=1,
+                              source_point=[7, 13, 15], source_wavelet=wav)
+    prob = P.make_wave_problem(cfg)
+    res = P.run(prob, form=form)
+    ref = O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=1, source_point=[7, 13, 15],
+                                    source_wavelet=wav))
+    nz = np.argwhere(res.u.data[1] != 0)
+    assert nz.tolist() == [[7, 13, 15]]
+    assert res.u.data[1][7, 13, 15] == ref["levels"][1][7, 13, 15]
+
+
+@pytest.mark.parametrize("form", ["factorised", "plain_f64"])
+def test_receiver_indexing_bit_exact(form):
+    shape, so, nt = (24, 24, 24), 4, 6
+    wav = np.linspace(0.0, 1.0, nt).astype(np.float32)
+    rec = np.array([[x, y, z] for x in (11, 12) for y in (3, 12) for z in (2, 12, 21)], np.int32)
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
+                              source_wavelet=wav)
+    res = P.run(P.make_wave_problem(cfg), form=form, receivers=rec)
+    # traces must be exactly the newest level at the receiver points (on_step semantics)
+    assert np.array_equal(res.rec_traces[-1], res.u.data[nt % 3][tuple(rec.T)])
+    ref = O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=nt, source_wavelet=wav),
+                     receivers=rec)
+    if form == "plain_f64":
+        assert np.array_equal(res.rec_traces, ref["rec_traces"])
+    else:
+        assert rel_l2(res.rec_traces, ref["rec_traces"]) <= TOL
+
+
+def test_instability_error_step_matches_reference():
+    cfg = P.WaveProblemConfig(shape=(16, 16, 16), spacing=(10.0, 10.0, 10.0), space_order=4,
+                              steps=400, dt=0.02)
+    with pytest.raises(P.InstabilityError) as ei:
+        P.run(P.make_wave_problem(cfg), dse=P.DseLevel.basic)
+    with pytest.raises(O.OracleError) as eo:
+        O.port_run(O.OracleConfig(shape=(16, 16, 16), space_order=4, steps=400, dt=0.02))
+    assert ei.value.step() == eo.value.step >= 0
+
+
+@pytest.mark.parametrize("form", ["factorised", "plain_f64"])
+def test_apply_is_resumable(form):
+    cfg = P.WaveProblemConfig(shape=(20, 21, 22), spacing=(10.0, 10.0, 10.0), space_order=6, steps=12)
+    prob = P.make_wave_problem(cfg)
+    a = P.Operator(prob, form=form)
+    a.apply(12, 0)
+    b = P.Operator(prob, form=form)
+    b.apply(5, 0)
+    b.apply(7)
+    assert np.array_equal(a.levels(), b.levels())
+
+
+@pytest.mark.parametrize("form", ["factorised", "plain_f64", "factorised_simple"])
+@pytest.mark.parametrize("cuts", [(13,), (9, 18), (6, 11, 20)])
+def test_local_slabs_bitwise_equal_single_domain(form, cuts):
+    """z-slab decomposition (reference dim 0) with SO/2 ghost planes written by the
+    neighbours' stencil kernels: N slabs == 1 domain, bit for bit."""
+    shape, so, nt = (28, 20, 22), 8, 9
+    rng = np.random.default_rng(3)
+    vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
+                              velocity_field=vel, damp_max=0.05, damp_width=4,
+                              source_point=[12, 10, 11])
+    prob = P.make_wave_problem(cfg)
+    rec = np.array([[x, 10, 11] for x in range(shape[0])], np.int32)
+    whole = P.Operator(prob, form=form, receivers=rec)
+    wr = whole.apply(nt, 0)
+    bounds = [0] + list(cuts) + [shape[0]]
+    ops = [P.Operator(prob, form=form, receivers=rec, slab=(bounds[i], bounds[i + 1]))
+           for i in range(len(bounds) - 1)]
+    for lo, hi in zip(ops[:-1], ops[1:]):
+        P.Operator.link_local(lo, hi)
+    for o in ops:
+        o.apply_async(nt, 0)
+    smax = np.max([o.collect(nt) for o in ops], axis=0)
+    assert np.array_equal(smax, wr.step_max_abs)
+    for l in range(3):
+        full = np.zeros(shape, np.float32)
+        for o in ops:
+            part = o.get_level(l)
+            lo_, hi_ = o.slab
+            full[lo_:hi_] = part[lo_:hi_]
+        assert np.array_equal(full, whole.get_level(l)), l
