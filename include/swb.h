@@ -51,13 +51,15 @@ extern "C" {
  * SWB_FORM_PLAIN_F64  : basic form evaluated exactly as the interpreter does (double,
  *                       same term order, one division per product, no FMA): bit-exact.
  * SWB_FORM_PLAIN_F32  : basic form in FP32 term by term (the paper's OPS kernel, src/opsgen.cpp:327-355).
- * SWB_FORM_FACTORISED_SIMPLE : same arithmetic as FACTORISED, one thread per point, no TMA
- *                       (kernel-choice baseline). */
+ * SWB_FORM_FACTORISED_SIMPLE : FP32 Laplacian + FP64 combine, one thread per point, no TMA
+ *                       (kernel-choice baseline).
+ * SWB_FORM_FACTORISED_SIMPLE_F32C : same, with the all-FP32 combine of the TMA kernel. */
 enum swb_form {
     SWB_FORM_FACTORISED = 0,
     SWB_FORM_PLAIN_F64 = 1,
     SWB_FORM_PLAIN_F32 = 2,
-    SWB_FORM_FACTORISED_SIMPLE = 3
+    SWB_FORM_FACTORISED_SIMPLE = 3,
+    SWB_FORM_FACTORISED_SIMPLE_F32C = 4
 };
 
 /* Everything exec::run reads from WaveProblem + the IET (src/executor.cpp:189-199, 383-403,

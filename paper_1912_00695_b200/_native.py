@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libswb.so")
 
 SWB_OK, SWB_EINVAL, SWB_ECUDA, SWB_EUNSTABLE = 0, 1, 2, 3
 FORM_FACTORISED, FORM_PLAIN_F64, FORM_PLAIN_F32, FORM_FACTORISED_SIMPLE = 0, 1, 2, 3
+FORM_FACTORISED_SIMPLE_F32C = 4
 
 
 class SwbProblem(C.Structure):

@@ -132,6 +132,19 @@ __device__ __forceinline__ float combine_f64(const Coef& K, double L, float u0, 
     return static_cast<float>(num / (a + b));
 }
 
+// FP32 combine with no systematic coefficient rounding:
+//   u+ - u = [ (m - g)(u - up) + Lr*(dt/h)^2 ] / (m + g),   g = damp*dt/2,
+// where Lr = S + 3R*u is the raw (unscaled) Laplacian sum and (dt/h)^2 is applied as an
+// exact hi+lo float pair; the quotient is an IEEE division and the final add is the only
+// rounding at the scale of u (the interpreter's one final store rounding).
+__device__ __forceinline__ float combine_f32(float Lr, float u0, float up, float m, float dmp,
+                                             float kap_hi, float kap_lo, float half_dt) {
+    const float Lk = fmaf(Lr, kap_hi, Lr * kap_lo);
+    const float g = dmp * half_dt;
+    const float num = fmaf(m - g, u0 - up, Lk);
+    return u0 + __fdiv_rn(num, m + g);
+}
+
 __device__ __forceinline__ double lap_total(const Coef& K, float s0, float s1, float s2, float u0) {
     if (K.iso) {
         const float s = (s0 + s1) + s2;

@@ -33,7 +33,12 @@ __global__ void __launch_bounds__(128) k_simple(Geo g, Coef K, Ctl c, Peer p) {
             const float sx = lap_axis<H>(K, u0, [&](int k) { return ut[i + k * s0]; });
             const float sy = lap_axis<H>(K, u0, [&](int k) { return ut[i + k * s1]; });
             const float sz = lap_axis<H>(K, u0, [&](int k) { return ut[i + k]; });
-            v = combine_f64(K, lap_total(K, sx, sy, sz, u0), u0, up, m, dmp);
+            if (FORM == 3 && K.iso) {
+                const float Lr = fmaf(K.R3, u0, (sx + sy) + sz);
+                v = combine_f32(Lr, u0, up, m, dmp, K.kap_hi, K.kap_lo, K.half_dt);
+            } else {
+                v = combine_f64(K, lap_total(K, sx, sy, sz, u0), u0, up, m, dmp);
+            }
         }
         if (c.has_src && x == c.src_x && y == c.src_y && z == c.src_z)
             v = inject_source(v, c.wavelet[c.step], m, static_cast<double>(K.dt));
@@ -56,6 +61,7 @@ static cudaError_t launch_simple_h(int form, const Geo& g, const Coef& K, const 
     switch (form) {
         case 1: k_simple<H, 1><<<grid, block, 0, s>>>(g, K, c, p); break;
         case 2: k_simple<H, 2><<<grid, block, 0, s>>>(g, K, c, p); break;
+        case 3: k_simple<H, 3><<<grid, block, 0, s>>>(g, K, c, p); break;
         default: k_simple<H, 0><<<grid, block, 0, s>>>(g, K, c, p); break;
     }
     return cudaGetLastError();

@@ -27,7 +27,8 @@ struct TmaPlan {
 };
 TmaPlan tma_plan(int H, const Geo& g, int num_sms);
 // Encodes the tensor maps for the three u levels (once per handle).
-cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*3 x 128 B*/);
+constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps
+cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*kTmaMapsBytes*/);
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s);
 

@@ -72,7 +72,7 @@ struct swb_handle {
     Ctl ctl{};
     Peer peer{};
     TmaPlan plan{};
-    alignas(128) unsigned char maps[3 * 128];
+    alignas(128) unsigned char maps[kTmaMapsBytes];
     bool use_tma = false;
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
@@ -126,6 +126,12 @@ void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
     K.half_inv_dt = 0.5 / dt;
     K.inject = dt * dt;
     K.iso = (p->spacing[0] == p->spacing[1] && p->spacing[1] == p->spacing[2]) ? 1 : 0;
+    K.R3 = static_cast<float>(3.0 * K.R_d);
+    const double h0 = static_cast<double>(p->spacing[0]);
+    const double kap = (dt / h0) * (dt / h0);
+    K.kap_hi = static_cast<float>(kap);
+    K.kap_lo = static_cast<float>(kap - static_cast<double>(K.kap_hi));
+    K.half_dt = static_cast<float>(0.5 * dt);
 }
 
 int ensure_smax(swb_handle* h, int nt) {
@@ -179,7 +185,10 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
         if (h->use_tma) {
             SWB_CUDA(launch_tma(h->plan, h->maps, h->geo, h->K, c, h->peer, h->stream));
         } else {
-            const int form = h->form == SWB_FORM_PLAIN_F64 ? 1 : h->form == SWB_FORM_PLAIN_F32 ? 2 : 0;
+            const int form = h->form == SWB_FORM_PLAIN_F64   ? 1
+                             : h->form == SWB_FORM_PLAIN_F32 ? 2
+                             : h->form == SWB_FORM_FACTORISED_SIMPLE_F32C ? 3
+                                                                     : 0;
             SWB_CUDA(launch_simple(h->H, form, h->geo, h->K, c, h->peer, h->stream));
         }
         ++h->launches;
@@ -243,7 +252,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         return fail(SWB_EINVAL, "space_order above 24 is not supported");
     if (!(p->dt > 0.0f)) return fail(SWB_EINVAL, "dt must be positive");
     if (!p->m) return fail(SWB_EINVAL, "m (squared slowness) is required");
-    if (p->form < 0 || p->form > 3) return fail(SWB_EINVAL, "unknown stencil form");
+    if (p->form < 0 || p->form > 4) return fail(SWB_EINVAL, "unknown stencil form");
     if (p->time_block < 0) return fail(SWB_EINVAL, "time_block must be >= 1");
     const int HU = p->space_order / 2;
     const int H = std::max(HU, 1);  // widest halo among u (SO/2), m and damp (1): src/pipeline.cpp:79-88

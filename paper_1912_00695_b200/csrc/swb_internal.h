@@ -39,6 +39,9 @@ struct Coef {
     double inv_dt2;         // 1 / (double(dt)^2)
     double half_inv_dt;     // 0.5 / double(dt)
     double inject;          // double(dt) * double(dt)   (source scale numerator)
+    float R3;               // fp32(3 (c0 + 2 c1))  (isotropic residual)
+    float kap_hi, kap_lo;   // (dt/h)^2 as an exact-ish float pair (isotropic)
+    float half_dt;          // dt/2 (exact)
     int iso;                // h[0]==h[1]==h[2]
 };
 

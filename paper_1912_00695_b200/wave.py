@@ -299,7 +299,8 @@ class RunResult:
 
 
 _FORMS = {"factorised": N.FORM_FACTORISED, "plain_f64": N.FORM_PLAIN_F64,
-          "plain_f32": N.FORM_PLAIN_F32, "factorised_simple": N.FORM_FACTORISED_SIMPLE}
+          "plain_f32": N.FORM_PLAIN_F32, "factorised_simple": N.FORM_FACTORISED_SIMPLE,
+          "factorised_simple_f32c": N.FORM_FACTORISED_SIMPLE_F32C}
 
 
 def form_for(dse: DseLevel) -> str:
