@@ -47,8 +47,9 @@ struct Maps {
 struct Sched {
     int nyt, nzt, ncol;   // column tiles
     int np;               // planes to update per column
-    long long work;       // ncol * np
+    int nchunk;           // dim-0 chunks per column (work items = ncol * nchunk)
     int y0, y1, z0, z1, zs, x0;
+    const unsigned char* dflag;  // [ncol][np]: damp tile non-zero (null = always load damp)
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -81,6 +82,14 @@ __device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, 
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_load3_hint(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                               int c2, unsigned bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -101,26 +110,6 @@ __device__ __forceinline__ void set_comp(float4& v, int e, float x) {
     else v.w = x;
 }
 
-// Walk the segments [col, p_lo, p_hi) of this CTA's balanced work range.
-struct SegIter {
-    long long u, end;
-    int np;
-    __device__ SegIter(long long work, int np_, int cta, int ncta) : np(np_) {
-        u = work * cta / ncta;
-        end = work * (cta + 1) / ncta;
-    }
-    __device__ bool next(int& col, int& pa, int& pb) {
-        if (u >= end) return false;
-        col = static_cast<int>(u / np);
-        pa = static_cast<int>(u % np);
-        const long long cend = static_cast<long long>(col + 1) * np;
-        const long long e = end < cend ? end : cend;
-        pb = static_cast<int>(e - static_cast<long long>(col) * np);
-        u = e;
-        return true;
-    }
-};
-
 template <int H, int R1, int T1>
 struct Cfg {
     static constexpr int A = (H + 3) / 4 * 4;         // dim-2 halo rounded to float4
@@ -132,6 +121,30 @@ struct Cfg {
     static constexpr int NTHREADS = 32 * (NCW + 1);
     static constexpr int NQ = 2 * H + 1;               // queue depth
 };
+
+// ---- packed FP32x2 arithmetic (FADD2 / FFMA2 / FMUL2 on sm_100a) --------------------
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    return __ffma2_rn(b, make_float2(-1.f, -1.f), a);  // a - b, one rounding
+}
+__device__ __forceinline__ float2 splat(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// n / d with one Newton step on MUFU.RCP: error <= 1 ulp of the quotient (the quotient is the
+// per-step increment, ~0.1 |u|, so this is ~0.1 ulp of u; see DESIGN.md numerics).
+__device__ __forceinline__ float2 div2(float2 n, float2 d) {
+    const float2 r = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+    const float2 q = mul2(n, r);
+    const float2 e = fma2(make_float2(-d.x, -d.y), q, n);
+    return fma2(e, r, q);
+}
 
 template <int H, int R1, int T1, int SU, int SA>
 __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
@@ -161,7 +174,8 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     __syncthreads();
 
     const int lt = c.step % 3, ln = (c.step + 1) % 3, lp = (c.step + 2) % 3;
-    const int ncta = gridDim.x;
+    const int G = gridDim.x;
+    const int nitems = sc.ncol * sc.nchunk;
     unsigned mine = 0u;
 
     if (warp == 0) {
@@ -173,29 +187,39 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             prefetch_map(ma);
             prefetch_map(&maps.m);
             prefetch_map(&maps.damp);
+            uint64_t pol_first;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
             constexpr int DA = SA - 1 < 2 ? SA - 1 : 2;  // aux prefetch distance (planes)
             unsigned nu = 0, na = 0;
-            SegIter it(sc.work, sc.np, blockIdx.x, ncta);
-            int col, pa, pb;
-            while (it.next(col, pa, pb)) {
+            for (int item = blockIdx.x; item < nitems; item += G) {
+                const int col = item % sc.ncol, chunk = item / sc.ncol;
+                const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
+                const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+                const int dir = (chunk & 1) ? 1 : -1;   // even chunks descend, odd ascend
+                const int q0 = dir > 0 ? xa - H : xb - 1 + H;
+                const int nq = xb - xa + 2 * H;
                 const int yt = sc.y0 + (col / sc.nzt) * T1;
                 const int zt = sc.zs + (col % sc.nzt) * kT2;
-                const int xa = sc.x0 + pa, xb = sc.x0 + pb;  // local output planes [xa, xb)
-                for (int q = xa - H; q < xb + H; ++q) {
+                const unsigned char* dfl = sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
+                for (int j = 0; j < nq; ++j) {
+                    const int q = q0 + dir * j;
                     const unsigned st = nu % SU, ph = (nu / SU) & 1u;
                     mbar_wait(empty_u + 8 * st, ph ^ 1u);
                     mbar_expect_tx(full_u + 8 * st, C::ROWS * C::W2 * 4);
                     tma_load3(uring_s + st * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * st);
                     ++nu;
-                    const int p = q - H + DA;
+                    const int p = q - dir * (H - DA);
                     if (p >= xa && p < xb) {
                         const unsigned sa = na % SA, pha = (na / SA) & 1u;
                         mbar_wait(empty_a + 8 * sa, pha ^ 1u);
-                        mbar_expect_tx(full_a + 8 * sa, 3 * C::ATILE);
+                        const bool need_damp = !dfl || dfl[p];
+                        mbar_expect_tx(full_a + 8 * sa, (need_damp ? 3 : 2) * C::ATILE);
                         const unsigned dst = aring_s + sa * 3 * C::ATILE;
-                        tma_load3(dst, ma, zt, yt, p, full_a + 8 * sa);
-                        tma_load3(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * sa);
-                        tma_load3(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * sa);
+                        tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * sa, pol_first);
+                        tma_load3_hint(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * sa, pol_first);
+                        if (need_damp)
+                            tma_load3_hint(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * sa,
+                                           pol_first);
                         ++na;
                     }
                 }
@@ -210,28 +234,37 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         float* un = pick3(g.lev[0], g.lev[1], g.lev[2], ln);
         float* lo_peer = pick3(pr.lo_lev[0], pr.lo_lev[1], pr.lo_lev[2], ln);
         float* hi_peer = pick3(pr.hi_lev[0], pr.hi_lev[1], pr.hi_lev[2], ln);
+        const float* ushm = reinterpret_cast<const float*>(uring);
+        const float* ashm = reinterpret_cast<const float*>(aring);
+        const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+        const float2 hdt = splat(K.half_dt);
         float4 Q[R1][C::NQ];  // register queue along dim 0
         unsigned nu = 0, na = 0;
-        SegIter it(sc.work, sc.np, blockIdx.x, ncta);
-        int col, pa, pb;
-        while (it.next(col, pa, pb)) {
+        for (int item = blockIdx.x; item < nitems; item += G) {
+            const int col = item % sc.ncol, chunk = item / sc.ncol;
+            const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
+            const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+            const int dir = (chunk & 1) ? 1 : -1;
+            const int q0 = dir > 0 ? xa - H : xb - 1 + H;
+            const int nq = xb - xa + 2 * H;
             const int yt = sc.y0 + (col / sc.nzt) * T1;
             const int zt = sc.zs + (col % sc.nzt) * kT2;
-            const int xa = sc.x0 + pa, xb = sc.x0 + pb;
+            const unsigned char* dfl = sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
             const int zc = zt + 4 * tz;  // first z of this thread's float4
-            const unsigned base_u = nu;  // sequence number of plane xa - H
+            const unsigned base_u = nu;  // sequence number of plane q0
+            const bool zfull = zc >= sc.z0 && zc + 3 < sc.z1;
 #pragma unroll 1
-            for (int q = xa - H; q < xb + H; ++q) {
+            for (int j = 0; j < nq; ++j) {
+                const int q = q0 + dir * j;
                 const unsigned st = nu % SU, ph = (nu / SU) & 1u;
                 mbar_wait(full_u + 8 * st, ph);
-                const unsigned plane_q = uring_s + st * C::UPLANE;
-                // shift the queue and append the centre values of plane q
+                const float* plane_q = ushm + st * (C::UPLANE / 4);
 #pragma unroll
                 for (int i = 0; i < R1; ++i) {
 #pragma unroll
                     for (int k = 0; k < C::NQ - 1; ++k) Q[i][k] = Q[i][k + 1];
-                    Q[i][C::NQ - 1] =
-                        lds4(plane_q + 4 * ((r0 + i + H) * C::W2 + C::A + 4 * tz));
+                    Q[i][C::NQ - 1] = *reinterpret_cast<const float4*>(
+                        plane_q + (r0 + i + H) * C::W2 + C::A + 4 * tz);
                 }
                 ++nu;
                 const bool keep = q >= xa && q < xb;  // needed later for an in-plane stencil
@@ -239,78 +272,87 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(empty_u + 8 * st);
                 }
-                const int p = q - H;
-                if (p < xa) continue;
+                if (j < 2 * H) continue;
+                const int p = q - dir * H;
                 // ---- output plane p: in-plane stencil from its smem stage ----
-                const unsigned sp = (base_u + static_cast<unsigned>(p - (xa - H))) % SU;
-                const unsigned plane_p = uring_s + sp * C::UPLANE;
-                float4 acc[R1];
-#pragma unroll
-                for (int i = 0; i < R1; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                // far terms (k >= 2): dim 0 from the queue, dim 1 / dim 2 from smem
-#pragma unroll
-                for (int k = H; k >= 2; --k) {
-                    const float ck = K.c[k];
-#pragma unroll
-                    for (int i = 0; i < R1; ++i) {
-                        const float4 a0 = Q[i][H - k], b0 = Q[i][H + k];
-                        const float4 a1 = lds4(plane_p + 4 * ((r0 + i + H - k) * C::W2 + C::A + 4 * tz));
-                        const float4 b1 = lds4(plane_p + 4 * ((r0 + i + H + k) * C::W2 + C::A + 4 * tz));
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float s = (comp(a0, e) + comp(b0, e)) + (comp(a1, e) + comp(b1, e));
-                            set_comp(acc[i], e, fmaf(ck, s, comp(acc[i], e)));
-                        }
-                    }
-                }
-                // dim 2 far terms from a (4 + 2A)-wide window of the centre row
+                const unsigned sp = (base_u + static_cast<unsigned>(j - 2 * H + H)) % SU;
+                const float* pp = ushm + sp * (C::UPLANE / 4);
+                float2 acc[R1][2];
 #pragma unroll
                 for (int i = 0; i < R1; ++i) {
+                    // dim 0 (queue) + dim 1 (rows) + dim 2 (window), far terms k >= 2
+                    const float* rowc = pp + (r0 + i + H) * C::W2;
                     float w[4 + 2 * C::A];
 #pragma unroll
-                    for (int j = 0; j < (4 + 2 * C::A) / 4; ++j) {
-                        const float4 v = lds4(plane_p + 4 * ((r0 + i + H) * C::W2 + 4 * tz + 4 * j));
-                        w[4 * j] = v.x;
-                        w[4 * j + 1] = v.y;
-                        w[4 * j + 2] = v.z;
-                        w[4 * j + 3] = v.w;
+                    for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
+                        const float4 v = *reinterpret_cast<const float4*>(rowc + 4 * tz + 4 * jj);
+                        w[4 * jj] = v.x;
+                        w[4 * jj + 1] = v.y;
+                        w[4 * jj + 2] = v.z;
+                        w[4 * jj + 3] = v.w;
                     }
-                    const float4 u0 = Q[i][H];
+                    float2 al = splat(0.f), ah = splat(0.f);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        float a = comp(acc[i], e);
-#pragma unroll
-                        for (int k = H; k >= 2; --k)
-                            a = fmaf(K.c[k], w[C::A + e - k] + w[C::A + e + k], a);
-                        const float uc = comp(u0, e);
-                        // k = 1 ring of all three axes in difference form
-                        const float4 xm = Q[i][H - 1], xp = Q[i][H + 1];
-                        float d1 = (comp(xm, e) - uc) + (comp(xp, e) - uc);
-                        d1 += (w[C::A + e - 1] - uc) + (w[C::A + e + 1] - uc);
-                        set_comp(acc[i], e, a);
-                        // dim 1 k=1 handled below (needs the neighbour rows)
-                        set_comp(acc[i], e, fmaf(K.c[1], d1, comp(acc[i], e)));
+                    for (int k = H; k >= 2; --k) {
+                        const float2 ck = splat(K.c[k]);
+                        const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2 + C::A + 4 * tz);
+                        const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2 + C::A + 4 * tz);
+                        const float4& xm = Q[i][H - k];
+                        const float4& xp = Q[i][H + k];
+                        float2 zl, zh;
+                        if ((k & 1) == 0) {  // register-pair aligned: packed adds
+                            zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]),
+                                      make_float2(w[C::A + k], w[C::A + 1 + k]));
+                            zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
+                                      make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
+                        } else {
+                            zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
+                            zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k],
+                                             w[C::A + 3 - k] + w[C::A + 3 + k]);
+                        }
+                        const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
+                        const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
+                        al = fma2(ck, sl, al);
+                        ah = fma2(ck, sh, ah);
                     }
-                    const float4 ym = lds4(plane_p + 4 * ((r0 + i + H - 1) * C::W2 + C::A + 4 * tz));
-                    const float4 yp = lds4(plane_p + 4 * ((r0 + i + H + 1) * C::W2 + C::A + 4 * tz));
+                    // k = 1 ring in difference form, all three axes
+                    {
+                        const float4 u0 = Q[i][H];
+                        const float4 ym = *reinterpret_cast<const float4*>(rowc - C::W2 + C::A + 4 * tz);
+                        const float4 yp = *reinterpret_cast<const float4*>(rowc + C::W2 + C::A + 4 * tz);
+                        const float4& xm = Q[i][H - 1];
+                        const float4& xp = Q[i][H + 1];
+                        const float2 ul = lo2(u0), uh = hi2(u0);
+                        float dz[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float uc = comp(u0, e);
-                        set_comp(acc[i], e,
-                                 fmaf(K.c[1], (comp(ym, e) - uc) + (comp(yp, e) - uc), comp(acc[i], e)));
+                        for (int e = 0; e < 4; ++e) {
+                            const float ue = comp(u0, e);
+                            dz[e] = (w[C::A + e - 1] - ue) + (w[C::A + e + 1] - ue);
+                        }
+                        float2 dl = add2(sub2(lo2(xm), ul), sub2(lo2(xp), ul));
+                        dl = add2(dl, add2(sub2(lo2(ym), ul), sub2(lo2(yp), ul)));
+                        dl = add2(dl, make_float2(dz[0], dz[1]));
+                        float2 dh = add2(sub2(hi2(xm), uh), sub2(hi2(xp), uh));
+                        dh = add2(dh, add2(sub2(hi2(ym), uh), sub2(hi2(yp), uh)));
+                        dh = add2(dh, make_float2(dz[2], dz[3]));
+                        const float2 c1 = splat(K.c[1]);
+                        acc[i][0] = fma2(c1, dl, al);
+                        acc[i][1] = fma2(c1, dh, ah);
                     }
                 }
                 // ---- aux tiles: u[t-1], m, damp ----
                 const unsigned sa = na % SA, pha = (na / SA) & 1u;
                 mbar_wait(full_a + 8 * sa, pha);
-                const unsigned aux = aring_s + sa * 3 * C::ATILE;
+                const float* aux = ashm + sa * (3 * C::ATILE / 4);
+                const bool has_damp = !dfl || dfl[p];
                 float4 upv[R1], mv[R1], dv[R1];
 #pragma unroll
                 for (int i = 0; i < R1; ++i) {
-                    const unsigned off = 4 * ((r0 + i) * kT2 + 4 * tz);
-                    upv[i] = lds4(aux + off);
-                    mv[i] = lds4(aux + C::ATILE + off);
-                    dv[i] = lds4(aux + 2 * C::ATILE + off);
+                    const int off = (r0 + i) * kT2 + 4 * tz;
+                    upv[i] = *reinterpret_cast<const float4*>(aux + off);
+                    mv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + off);
+                    dv[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + off)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -320,18 +362,26 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                 ++na;
                 // ---- combine + fused epilogue ----
                 const long long xoff = static_cast<long long>(p) * g.plane;
+                const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
+                const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
 #pragma unroll
                 for (int i = 0; i < R1; ++i) {
                     const int y = yt + r0 + i;
-                    float4 out;
+                    const float4 u0 = Q[i][H];
+                    float2 res[2];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float uc = comp(Q[i][H], e);
-                        const float Lr = fmaf(K.R3, uc, comp(acc[i], e));
-                        set_comp(out, e,
-                                 combine_f32(Lr, uc, comp(upv[i], e), comp(mv[i], e), comp(dv[i], e),
-                                             K.kap_hi, K.kap_lo, K.half_dt));
+                    for (int h = 0; h < 2; ++h) {
+                        const float2 uc = h ? hi2(u0) : lo2(u0);
+                        const float2 um = h ? hi2(upv[i]) : lo2(upv[i]);
+                        const float2 m = h ? hi2(mv[i]) : lo2(mv[i]);
+                        const float2 dm = h ? hi2(dv[i]) : lo2(dv[i]);
+                        const float2 Lr = fma2(R3, uc, acc[i][h]);
+                        const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
+                        const float2 gg = mul2(dm, hdt);
+                        const float2 num = fma2(sub2(m, gg), sub2(uc, um), Lk);
+                        res[h] = add2(uc, div2(num, add2(m, gg)));
                     }
+                    float4 out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
                     if (y < sc.y1) {
                         if (c.has_src && p == c.src_x && y == c.src_y &&
                             static_cast<unsigned>(c.src_z - zc) < 4u) {
@@ -340,10 +390,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                                                            comp(mv[i], e), static_cast<double>(K.dt)));
                         }
                         const long long idx = xoff + static_cast<long long>(y) * g.P2 + zc;
-                        const bool full = zc >= sc.z0 && zc + 3 < sc.z1;
-                        const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
-                        const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
-                        if (full) {
+                        if (zfull) {
                             *reinterpret_cast<float4*>(un + idx) = out;
                             if (lo_m)
                                 *reinterpret_cast<float4*>(
@@ -463,7 +510,14 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     const int np = g.x1 - g.x0;
     p.work = static_cast<long long>(p.columns) * np;
     if (np <= 0 || p.columns <= 0) return p;
-    p.grid = static_cast<int>(std::min<long long>(num_sms, p.work));
+    // Work items: column tiles x dim-0 chunks.  Chunk boundaries line up across columns and
+    // alternate direction (even chunks descend, odd ascend), so CTAs meeting at a chunk
+    // boundary read the shared planes at the same time (L2 hits), and neighbouring columns
+    // stream the same planes concurrently (halo re-reads hit L2).
+    int nchunk = std::max(1, num_sms / p.columns);
+    nchunk = std::min(nchunk, std::max(1, np / std::max(2, 2 * H)));
+    p.nchunk = nchunk;
+    p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * nchunk));
     p.variant = 1000 + H;
     if (cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(v->smem)) != cudaSuccess) {
@@ -492,6 +546,30 @@ cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* out)
 
 static_assert(sizeof(Maps) == kTmaMapsBytes, "tensor-map block size");
 
+void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp, int n1, int n2,
+                    unsigned char* flags) {
+    const int np = g.x1 - g.x0;
+    for (int col = 0; col < plan.columns; ++col) {
+        const int yt = g.y0 + (col / plan.tiles_z) * plan.T1;
+        const int zt = plan.zs + (col % plan.tiles_z) * kT2;
+        const int ya = yt, yb = std::min(yt + plan.T1, g.y1);
+        const int za = std::max(zt, g.z0), zb = std::min(zt + kT2, g.z1);
+        for (int x = g.x0; x < g.x1; ++x) {
+            unsigned char f = 0;
+            if (damp) {
+                const float* pl = damp + static_cast<long long>(x + g.xg_off) * n1 * n2;
+                for (int y = ya; y < yb && !f; ++y)
+                    for (int z = za; z < zb; ++z)
+                        if (pl[static_cast<long long>(y) * n2 + z] != 0.0f) {
+                            f = 1;
+                            break;
+                        }
+            }
+            flags[static_cast<long long>(col) * np + (x - g.x0)] = f;
+        }
+    }
+}
+
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s) {
     const Variant* v = find_variant(plan.H);
@@ -501,7 +579,8 @@ cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, cons
     sc.nzt = plan.tiles_z;
     sc.ncol = plan.columns;
     sc.np = g.x1 - g.x0;
-    sc.work = plan.work;
+    sc.nchunk = plan.nchunk;
+    sc.dflag = plan.dflag;
     sc.y0 = g.y0;
     sc.y1 = g.y1;
     sc.z0 = g.z0;

@@ -23,8 +23,13 @@ struct TmaPlan {
     int zs;               // first (aligned) dim-2 column of tile 0
     int grid;             // persistent CTAs
     long long work;       // column tiles x planes
+    int nchunk;           // dim-0 chunks per column
+    const unsigned char* dflag;  // device [columns][planes] damp-tile-nonzero flags (or null)
     int variant;
 };
+// Host-side damp tile flags for a plan: flags[col * np + (x - x0)] = any damp != 0 in the tile.
+void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_local, int n1, int n2,
+                    unsigned char* flags);
 TmaPlan tma_plan(int H, const Geo& g, int num_sms);
 // Encodes the tensor maps for the three u levels (once per handle).
 constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps

@@ -74,6 +74,7 @@ struct swb_handle {
     TmaPlan plan{};
     alignas(128) unsigned char maps[kTmaMapsBytes];
     bool use_tma = false;
+    unsigned char* d_dflag = nullptr;
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
     unsigned long long* lo_remote = nullptr; // lower neighbour's d_flags[1]
@@ -407,8 +408,14 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
         h->plan = tma_plan(HU, g, sms);
-        if (h->plan.ok) {
+        if (h->plan.ok && h->K.iso) {
             SWB_CUDA_C(tma_make_maps(h->plan, g, h->nl0, h->maps));
+            const size_t nflags = static_cast<size_t>(h->plan.columns) * std::max(0, g.x1 - g.x0);
+            std::vector<unsigned char> flags(nflags);
+            tma_damp_flags(h->plan, g, p->damp, h->n1, h->n2, flags.data());
+            SWB_CUDA_C(cudaMalloc(&h->d_dflag, std::max<size_t>(nflags, 1)));
+            SWB_CUDA_C(cudaMemcpy(h->d_dflag, flags.data(), nflags, cudaMemcpyHostToDevice));
+            h->plan.dflag = h->d_dflag;
             h->use_tma = true;
         }
     }
@@ -553,7 +560,8 @@ int swb_destroy(swb_handle* h) {
     for (void* q : {static_cast<void*>(h->u), static_cast<void*>(h->m), static_cast<void*>(h->damp),
                     static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
                     static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
-                    static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags)})
+                    static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
+                    static_cast<void*>(h->d_dflag)})
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
