@@ -146,14 +146,229 @@ __device__ __forceinline__ float2 div2(float2 n, float2 d) {
     return fma2(e, r, q);
 }
 
+// Advance a ring position (stage, phase) by one.
+template <int S>
+__device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {
+    if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+    }
+}
+
+// Per-item state shared by the consumer's per-plane steps.
+struct Item {
+    int xa, xb, dir, q0, nq, yt, zc;
+    bool zfull, rows_ok;
+    long long gcol;
+};
+
+// One arrival step of a consumer thread: take plane q's centre values into queue slot U,
+// and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
+// (U - H) mod NQ.  All queue indices are compile-time.
+template <int H, int R1, int T1, int SU, int SA, int U>
+__device__ __forceinline__ void consumer_step(float4 (&Q)[R1][2 * H + 1], int j, const Item& it,
+                                              const float* ucol, const float* acol,
+                                              const unsigned* aflag, unsigned full_u,
+                                              unsigned empty_u, unsigned full_a, unsigned empty_a,
+                                              unsigned& su, unsigned& pu, unsigned& sp,
+                                              unsigned& sa, unsigned& pa_, unsigned& mine,
+                                              float* un, float* lo_peer, float* hi_peer,
+                                              const Geo& g, const Coef& K, const Ctl& c,
+                                              const Peer& pr) {
+    using C = Cfg<H, R1, T1>;
+    constexpr int NQ = 2 * H + 1;
+    const int q = it.q0 + it.dir * j;
+    mbar_wait(full_u + 8 * su, pu);
+    const float* plane_q = ucol + su * (C::UPLANE / 4);
+#pragma unroll
+    for (int i = 0; i < R1; ++i) Q[i][U] = *reinterpret_cast<const float4*>(plane_q + i * C::W2);
+    if (!(q >= it.xa && q < it.xb))  // only needed for its centre values
+        mbar_arrive(empty_u + 8 * su);
+    ring_next<SU>(su, pu);
+    if (j < 2 * H) return;
+    // ---- output plane p (arrived H planes ago, smem stage sp) ----
+    const int p = q - it.dir * H;
+    constexpr int UC = (U + NQ - H) % NQ;  // queue slot of plane p
+    const float* pp = ucol + sp * (C::UPLANE / 4);
+    float2 acc[R1][2];
+#pragma unroll
+    for (int i = 0; i < R1; ++i) {
+        const float* rowc = pp + i * C::W2;
+        float w[4 + 2 * C::A];
+#pragma unroll
+        for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
+            const float4 v = *reinterpret_cast<const float4*>(rowc - C::A + 4 * jj);
+            w[4 * jj] = v.x;
+            w[4 * jj + 1] = v.y;
+            w[4 * jj + 2] = v.z;
+            w[4 * jj + 3] = v.w;
+        }
+        float2 al = splat(0.f), ah = splat(0.f);
+#pragma unroll
+        for (int k = H; k >= 2; --k) {
+            const float2 ck = splat(K.c[k]);
+            const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2);
+            const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2);
+            const float4& xm = Q[i][(UC + NQ - k) % NQ];
+            const float4& xp = Q[i][(UC + k) % NQ];
+            float2 zl, zh;
+            if ((k & 1) == 0) {  // register-pair aligned: packed adds
+                zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]), make_float2(w[C::A + k], w[C::A + 1 + k]));
+                zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
+                          make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
+            } else {
+                zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
+                zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k], w[C::A + 3 - k] + w[C::A + 3 + k]);
+            }
+            const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
+            const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
+            al = fma2(ck, sl, al);
+            ah = fma2(ck, sh, ah);
+        }
+        // k = 1 ring in difference form, all three axes
+        const float4 u0 = Q[i][UC];
+        const float4 ym = *reinterpret_cast<const float4*>(rowc - C::W2);
+        const float4 yp = *reinterpret_cast<const float4*>(rowc + C::W2);
+        const float4& xm = Q[i][(UC + NQ - 1) % NQ];
+        const float4& xp = Q[i][(UC + 1) % NQ];
+        const float2 ul = lo2(u0), uh = hi2(u0);
+        float dz[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float ue = comp(u0, e);
+            dz[e] = (w[C::A + e - 1] - ue) + (w[C::A + e + 1] - ue);
+        }
+        float2 dl = add2(sub2(lo2(xm), ul), sub2(lo2(xp), ul));
+        dl = add2(dl, add2(sub2(lo2(ym), ul), sub2(lo2(yp), ul)));
+        dl = add2(dl, make_float2(dz[0], dz[1]));
+        float2 dh = add2(sub2(hi2(xm), uh), sub2(hi2(xp), uh));
+        dh = add2(dh, add2(sub2(hi2(ym), uh), sub2(hi2(yp), uh)));
+        dh = add2(dh, make_float2(dz[2], dz[3]));
+        const float2 c1 = splat(K.c[1]);
+        acc[i][0] = fma2(c1, dl, al);
+        acc[i][1] = fma2(c1, dh, ah);
+    }
+    // ---- aux tiles: u[t-1], m, damp ----
+    mbar_wait(full_a + 8 * sa, pa_);
+    const float* aux = acol + sa * (3 * C::ATILE / 4);
+    const bool has_damp = aflag[sa] != 0u;
+    float4 upv[R1], mv[R1], dv[R1];
+#pragma unroll
+    for (int i = 0; i < R1; ++i) {
+        upv[i] = *reinterpret_cast<const float4*>(aux + i * kT2);
+        mv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + i * kT2);
+        dv[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + i * kT2)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    mbar_arrive(empty_a + 8 * sa);
+    mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
+    ring_next<SA>(sa, pa_);
+    if (++sp == SU) sp = 0;
+    // ---- combine ----
+    const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+    const float2 hdt = splat(K.half_dt);
+    float4 out[R1];
+#pragma unroll
+    for (int i = 0; i < R1; ++i) {
+        const float4 u0 = Q[i][UC];
+        float2 res[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 ucv = h ? hi2(u0) : lo2(u0);
+            const float2 um = h ? hi2(upv[i]) : lo2(upv[i]);
+            const float2 m = h ? hi2(mv[i]) : lo2(mv[i]);
+            const float2 dm = h ? hi2(dv[i]) : lo2(dv[i]);
+            const float2 Lr = fma2(R3, ucv, acc[i][h]);
+            const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
+            const float2 gg = mul2(dm, hdt);
+            const float2 num = fma2(sub2(m, gg), sub2(ucv, um), Lk);
+            res[h] = add2(ucv, div2(num, add2(m, gg)));
+        }
+        out[i] = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
+    }
+    // ---- fused epilogue ----
+    const long long xoff = static_cast<long long>(p) * g.plane + it.gcol;
+    const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
+    const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
+    const bool src_plane = c.has_src && p == c.src_x;
+    if (it.zfull && it.rows_ok && !(lo_m || hi_m || src_plane)) {
+        // fast path: full float4 rows, no injection, no peer copies
+#pragma unroll
+        for (int i = 0; i < R1; ++i) {
+            *reinterpret_cast<float4*>(un + xoff + static_cast<long long>(i) * g.P2) = out[i];
+            mine = max(mine, max(max(abs_bits(out[i].x), abs_bits(out[i].y)),
+                                 max(abs_bits(out[i].z), abs_bits(out[i].w))));
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < R1; ++i) {
+        const int y = it.yt + i;
+        float4 o = out[i];
+        if (y >= g.y1) continue;
+        if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
+            const int e = c.src_z - it.zc;
+            set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
+                                         static_cast<double>(K.dt)));
+        }
+        const long long idx = xoff + static_cast<long long>(i) * g.P2;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int z = it.zc + e;
+            if (z >= g.z0 && z < g.z1) {
+                const float v = comp(o, e);
+                un[idx + e] = v;
+                if (lo_m) lo_peer[idx + e + static_cast<long long>(pr.lo_shift) * g.plane] = v;
+                if (hi_m) hi_peer[idx + e + static_cast<long long>(pr.hi_shift) * g.plane] = v;
+                mine = max(mine, abs_bits(v));
+            }
+        }
+    }
+}
+
+template <int H, int R1, int T1, int SU, int SA, int U>
+struct Unrolled {
+    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + 1], int jb, const Item& it,
+                                               const float* ucol, const float* acol,
+                                               const unsigned* aflag, unsigned full_u, unsigned empty_u,
+                                               unsigned full_a, unsigned empty_a, unsigned& su,
+                                               unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
+                                               unsigned& mine, float* un, float* lo_peer,
+                                               float* hi_peer, const Geo& g, const Coef& K,
+                                               const Ctl& c, const Peer& pr) {
+        if (jb + U < it.nq) {
+            consumer_step<H, R1, T1, SU, SA, U>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
+                                                full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
+                                                lo_peer, hi_peer, g, K, c, pr);
+            Unrolled<H, R1, T1, SU, SA, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                                                    full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
+                                                    lo_peer, hi_peer, g, K, c, pr);
+        }
+    }
+};
+template <int H, int R1, int T1, int SU, int SA>
+struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
+    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + 1], int, const Item&,
+                                               const float*, const float*, const unsigned*, unsigned,
+                                               unsigned, unsigned, unsigned, unsigned&, unsigned&,
+                                               unsigned&, unsigned&, unsigned&, unsigned&, float*,
+                                               float*, float*, const Geo&, const Coef&, const Ctl&,
+                                               const Peer&) {}
+};
+
 template <int H, int R1, int T1, int SU, int SA>
 __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     k_tma(const __grid_constant__ Maps maps, Geo g, Coef K, Ctl c, Peer pr, Sched sc) {
     using C = Cfg<H, R1, T1>;
+    constexpr int NQ = C::NQ;
+    // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
+    // renaming; large halos: shift the queue (keeps the loop body small for the I-cache).
+    constexpr bool kUnroll = H <= 3;
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* uring = smem;
     unsigned char* aring = smem + SU * C::UPLANE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(aring + SA * 3 * C::ATILE);
+    unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA));  // damp-present per aux stage
     const unsigned full_u = smem_addr(bars), empty_u = full_u + 8 * SU;
     const unsigned full_a = empty_u + 8 * SU, empty_a = full_a + 8 * SA;
     const unsigned uring_s = smem_addr(uring), aring_s = smem_addr(aring);
@@ -162,11 +377,11 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < SU; ++i) {
             mbar_init(full_u + 8 * i, 1);
-            mbar_init(empty_u + 8 * i, C::NCW);
+            mbar_init(empty_u + 8 * i, 32 * C::NCW);  // every consumer thread arrives
         }
         for (int i = 0; i < SA; ++i) {
             mbar_init(full_a + 8 * i, 1);
-            mbar_init(empty_a + 8 * i, C::NCW);
+            mbar_init(empty_a + 8 * i, 32 * C::NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -190,7 +405,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             uint64_t pol_first;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
             constexpr int DA = SA - 1 < 2 ? SA - 1 : 2;  // aux prefetch distance (planes)
-            unsigned nu = 0, na = 0;
+            unsigned su = 0, pu = 0, sa = 0, pa_ = 0;
             for (int item = blockIdx.x; item < nitems; item += G) {
                 const int col = item % sc.ncol, chunk = item / sc.ncol;
                 const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
@@ -203,16 +418,15 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                 const unsigned char* dfl = sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
                 for (int j = 0; j < nq; ++j) {
                     const int q = q0 + dir * j;
-                    const unsigned st = nu % SU, ph = (nu / SU) & 1u;
-                    mbar_wait(empty_u + 8 * st, ph ^ 1u);
-                    mbar_expect_tx(full_u + 8 * st, C::ROWS * C::W2 * 4);
-                    tma_load3(uring_s + st * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * st);
-                    ++nu;
+                    mbar_wait(empty_u + 8 * su, pu ^ 1u);
+                    mbar_expect_tx(full_u + 8 * su, C::ROWS * C::W2 * 4);
+                    tma_load3(uring_s + su * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * su);
+                    ring_next<SU>(su, pu);
                     const int p = q - dir * (H - DA);
                     if (p >= xa && p < xb) {
-                        const unsigned sa = na % SA, pha = (na / SA) & 1u;
-                        mbar_wait(empty_a + 8 * sa, pha ^ 1u);
-                        const bool need_damp = !dfl || dfl[p];
+                        mbar_wait(empty_a + 8 * sa, pa_ ^ 1u);
+                        const unsigned need_damp = (!dfl || dfl[p]) ? 1u : 0u;
+                        aflag[sa] = need_damp;  // published by the arrive below (release)
                         mbar_expect_tx(full_a + 8 * sa, (need_damp ? 3 : 2) * C::ATILE);
                         const unsigned dst = aring_s + sa * 3 * C::ATILE;
                         tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * sa, pol_first);
@@ -220,7 +434,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                         if (need_damp)
                             tma_load3_hint(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * sa,
                                            pol_first);
-                        ++na;
+                        ring_next<SA>(sa, pa_);
                     }
                 }
             }
@@ -234,186 +448,43 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         float* un = pick3(g.lev[0], g.lev[1], g.lev[2], ln);
         float* lo_peer = pick3(pr.lo_lev[0], pr.lo_lev[1], pr.lo_lev[2], ln);
         float* hi_peer = pick3(pr.hi_lev[0], pr.hi_lev[1], pr.hi_lev[2], ln);
-        const float* ushm = reinterpret_cast<const float*>(uring);
-        const float* ashm = reinterpret_cast<const float*>(aring);
-        const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
-        const float2 hdt = splat(K.half_dt);
-        float4 Q[R1][C::NQ];  // register queue along dim 0
-        unsigned nu = 0, na = 0;
+        // this thread's column inside a u plane / an aux tile (floats)
+        const float* ucol = reinterpret_cast<const float*>(uring) + (r0 + H) * C::W2 + C::A + 4 * tz;
+        const float* acol = reinterpret_cast<const float*>(aring) + r0 * kT2 + 4 * tz;
+        float4 Q[R1][NQ];  // register queue along dim 0
+        unsigned su = 0, pu = 0, sp = 0, sa = 0, pa_ = 0;
         for (int item = blockIdx.x; item < nitems; item += G) {
             const int col = item % sc.ncol, chunk = item / sc.ncol;
-            const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
-            const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
-            const int dir = (chunk & 1) ? 1 : -1;
-            const int q0 = dir > 0 ? xa - H : xb - 1 + H;
-            const int nq = xb - xa + 2 * H;
-            const int yt = sc.y0 + (col / sc.nzt) * T1;
+            Item it;
+            it.xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
+            it.xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+            it.dir = (chunk & 1) ? 1 : -1;
+            it.q0 = it.dir > 0 ? it.xa - H : it.xb - 1 + H;
+            it.nq = it.xb - it.xa + 2 * H;
+            it.yt = sc.y0 + (col / sc.nzt) * T1 + r0;
             const int zt = sc.zs + (col % sc.nzt) * kT2;
-            const unsigned char* dfl = sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
-            const int zc = zt + 4 * tz;  // first z of this thread's float4
-            const unsigned base_u = nu;  // sequence number of plane q0
-            const bool zfull = zc >= sc.z0 && zc + 3 < sc.z1;
+            it.zc = zt + 4 * tz;  // first z of this thread's float4
+            it.zfull = it.zc >= sc.z0 && it.zc + 3 < sc.z1;
+            it.rows_ok = it.yt + R1 - 1 < sc.y1;
+            it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
+            sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
+            if constexpr (kUnroll) {
 #pragma unroll 1
-            for (int j = 0; j < nq; ++j) {
-                const int q = q0 + dir * j;
-                const unsigned st = nu % SU, ph = (nu / SU) & 1u;
-                mbar_wait(full_u + 8 * st, ph);
-                const float* plane_q = ushm + st * (C::UPLANE / 4);
+                for (int jb = 0; jb < it.nq; jb += NQ)
+                    Unrolled<H, R1, T1, SU, SA, 0>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                                                        full_a, empty_a, su, pu, sp, sa, pa_, mine,
+                                                        un, lo_peer, hi_peer, g, K, c, pr);
+            } else {
+#pragma unroll 1
+                for (int j = 0; j < it.nq; ++j) {
 #pragma unroll
-                for (int i = 0; i < R1; ++i) {
+                    for (int i = 0; i < R1; ++i)
 #pragma unroll
-                    for (int k = 0; k < C::NQ - 1; ++k) Q[i][k] = Q[i][k + 1];
-                    Q[i][C::NQ - 1] = *reinterpret_cast<const float4*>(
-                        plane_q + (r0 + i + H) * C::W2 + C::A + 4 * tz);
-                }
-                ++nu;
-                const bool keep = q >= xa && q < xb;  // needed later for an in-plane stencil
-                if (!keep) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty_u + 8 * st);
-                }
-                if (j < 2 * H) continue;
-                const int p = q - dir * H;
-                // ---- output plane p: in-plane stencil from its smem stage ----
-                const unsigned sp = (base_u + static_cast<unsigned>(j - 2 * H + H)) % SU;
-                const float* pp = ushm + sp * (C::UPLANE / 4);
-                float2 acc[R1][2];
-#pragma unroll
-                for (int i = 0; i < R1; ++i) {
-                    // dim 0 (queue) + dim 1 (rows) + dim 2 (window), far terms k >= 2
-                    const float* rowc = pp + (r0 + i + H) * C::W2;
-                    float w[4 + 2 * C::A];
-#pragma unroll
-                    for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
-                        const float4 v = *reinterpret_cast<const float4*>(rowc + 4 * tz + 4 * jj);
-                        w[4 * jj] = v.x;
-                        w[4 * jj + 1] = v.y;
-                        w[4 * jj + 2] = v.z;
-                        w[4 * jj + 3] = v.w;
-                    }
-                    float2 al = splat(0.f), ah = splat(0.f);
-#pragma unroll
-                    for (int k = H; k >= 2; --k) {
-                        const float2 ck = splat(K.c[k]);
-                        const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2 + C::A + 4 * tz);
-                        const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2 + C::A + 4 * tz);
-                        const float4& xm = Q[i][H - k];
-                        const float4& xp = Q[i][H + k];
-                        float2 zl, zh;
-                        if ((k & 1) == 0) {  // register-pair aligned: packed adds
-                            zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]),
-                                      make_float2(w[C::A + k], w[C::A + 1 + k]));
-                            zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
-                                      make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
-                        } else {
-                            zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
-                            zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k],
-                                             w[C::A + 3 - k] + w[C::A + 3 + k]);
-                        }
-                        const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
-                        const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
-                        al = fma2(ck, sl, al);
-                        ah = fma2(ck, sh, ah);
-                    }
-                    // k = 1 ring in difference form, all three axes
-                    {
-                        const float4 u0 = Q[i][H];
-                        const float4 ym = *reinterpret_cast<const float4*>(rowc - C::W2 + C::A + 4 * tz);
-                        const float4 yp = *reinterpret_cast<const float4*>(rowc + C::W2 + C::A + 4 * tz);
-                        const float4& xm = Q[i][H - 1];
-                        const float4& xp = Q[i][H + 1];
-                        const float2 ul = lo2(u0), uh = hi2(u0);
-                        float dz[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float ue = comp(u0, e);
-                            dz[e] = (w[C::A + e - 1] - ue) + (w[C::A + e + 1] - ue);
-                        }
-                        float2 dl = add2(sub2(lo2(xm), ul), sub2(lo2(xp), ul));
-                        dl = add2(dl, add2(sub2(lo2(ym), ul), sub2(lo2(yp), ul)));
-                        dl = add2(dl, make_float2(dz[0], dz[1]));
-                        float2 dh = add2(sub2(hi2(xm), uh), sub2(hi2(xp), uh));
-                        dh = add2(dh, add2(sub2(hi2(ym), uh), sub2(hi2(yp), uh)));
-                        dh = add2(dh, make_float2(dz[2], dz[3]));
-                        const float2 c1 = splat(K.c[1]);
-                        acc[i][0] = fma2(c1, dl, al);
-                        acc[i][1] = fma2(c1, dh, ah);
-                    }
-                }
-                // ---- aux tiles: u[t-1], m, damp ----
-                const unsigned sa = na % SA, pha = (na / SA) & 1u;
-                mbar_wait(full_a + 8 * sa, pha);
-                const float* aux = ashm + sa * (3 * C::ATILE / 4);
-                const bool has_damp = !dfl || dfl[p];
-                float4 upv[R1], mv[R1], dv[R1];
-#pragma unroll
-                for (int i = 0; i < R1; ++i) {
-                    const int off = (r0 + i) * kT2 + 4 * tz;
-                    upv[i] = *reinterpret_cast<const float4*>(aux + off);
-                    mv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + off);
-                    dv[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + off)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(empty_a + 8 * sa);
-                    mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
-                }
-                ++na;
-                // ---- combine + fused epilogue ----
-                const long long xoff = static_cast<long long>(p) * g.plane;
-                const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
-                const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
-#pragma unroll
-                for (int i = 0; i < R1; ++i) {
-                    const int y = yt + r0 + i;
-                    const float4 u0 = Q[i][H];
-                    float2 res[2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const float2 uc = h ? hi2(u0) : lo2(u0);
-                        const float2 um = h ? hi2(upv[i]) : lo2(upv[i]);
-                        const float2 m = h ? hi2(mv[i]) : lo2(mv[i]);
-                        const float2 dm = h ? hi2(dv[i]) : lo2(dv[i]);
-                        const float2 Lr = fma2(R3, uc, acc[i][h]);
-                        const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
-                        const float2 gg = mul2(dm, hdt);
-                        const float2 num = fma2(sub2(m, gg), sub2(uc, um), Lk);
-                        res[h] = add2(uc, div2(num, add2(m, gg)));
-                    }
-                    float4 out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
-                    if (y < sc.y1) {
-                        if (c.has_src && p == c.src_x && y == c.src_y &&
-                            static_cast<unsigned>(c.src_z - zc) < 4u) {
-                            const int e = c.src_z - zc;
-                            set_comp(out, e, inject_source(comp(out, e), c.wavelet[c.step],
-                                                           comp(mv[i], e), static_cast<double>(K.dt)));
-                        }
-                        const long long idx = xoff + static_cast<long long>(y) * g.P2 + zc;
-                        if (zfull) {
-                            *reinterpret_cast<float4*>(un + idx) = out;
-                            if (lo_m)
-                                *reinterpret_cast<float4*>(
-                                    lo_peer + idx + static_cast<long long>(pr.lo_shift) * g.plane) = out;
-                            if (hi_m)
-                                *reinterpret_cast<float4*>(
-                                    hi_peer + idx + static_cast<long long>(pr.hi_shift) * g.plane) = out;
-                            mine = max(mine, max(max(abs_bits(out.x), abs_bits(out.y)),
-                                                 max(abs_bits(out.z), abs_bits(out.w))));
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const int z = zc + e;
-                                if (z >= sc.z0 && z < sc.z1) {
-                                    const float v = comp(out, e);
-                                    un[idx + e] = v;
-                                    if (lo_m) lo_peer[idx + e + static_cast<long long>(pr.lo_shift) * g.plane] = v;
-                                    if (hi_m) hi_peer[idx + e + static_cast<long long>(pr.hi_shift) * g.plane] = v;
-                                    mine = max(mine, abs_bits(v));
-                                }
-                            }
-                        }
-                    }
+                        for (int k = 0; k < NQ - 1; ++k) Q[i][k] = Q[i][k + 1];
+                    consumer_step<H, R1, T1, SU, SA, NQ - 1>(Q, j, it, ucol, acol, aflag, full_u,
+                                                             empty_u, full_a, empty_a, su, pu, sp,
+                                                             sa, pa_, mine, un, lo_peer, hi_peer, g,
+                                                             K, c, pr);
                 }
             }
         }
@@ -426,7 +497,7 @@ template <int H, int R1, int T1, int SU, int SA>
 size_t smem_bytes() {
     using C = Cfg<H, R1, T1>;
     return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
-           16 * (SU + SA);
+           16 * (SU + SA) + 4 * SA;
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
