@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: the time-stepped 3-D acoustic FD operator on B200.
+
+Workload (BASELINE.json configs[1], the paper's roofline config): 3-D acoustic isotropic,
+256^3 grid per GPU, space order 8 (headline; SO 4/12/16 reported in "sweep"), h = 10 m,
+c = 1500 m/s, dt = cfl_dt, Ricker 10 Hz source at the centre, no damping.  A bench "step"
+is one time step of the operator over the whole grid.  With N GPUs the grid is
+256N x 256 x 256 in N z-slabs (reference dim 0) with the SO/2-plane halo exchange over
+NVLink peer memory (weak scaling).
+
+  value     GPts/s of the whole job, inputs resident in HBM, CUDA events on the operator's
+            stream, max over ranks
+  e2e       same metric through the public API with host buffers: handle creation (H2D of
+            m, damp, wavelet), H2D of the 3 initial levels from pinned memory, K steps, D2H of
+            the 3 final levels and the per-step max|u| (the exec::run contract)
+  roofline  algorithmic 20 B/point (read u[t], u[t-1], m, damp; write u[t+1]) / mean stencil
+            launch time vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the reference's own exec::run (basic IET, all host threads) on a bounded
+            sample of the same workload (rank 0, N=1)
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPts/s & % HBM roofline (3D acoustic, 256³, SO 4–16) at 1/2/4/8 B200 vs CPU"
+BYTES_PER_POINT = 20  # u[t], u[t-1], m, damp read + u[t+1] written, FP32
+FLOPS_AGGRESSIVE = {2: 24, 4: 34, 8: 57, 12: 75, 16: 93}  # reference's count_scalar_ops
+FLOPS_BASIC = {2: 69, 4: 105, 8: 165, 12: 225, 16: 285}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.2)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def traffic_from_profiles(so):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d["k_tma"][f"so{so}"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def pinned(shape):
+    import torch
+    return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_1912_00695_b200 as P
+    from paper_1912_00695_b200 import dist as D
+
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise SystemExit("no CUDA device")
+    device = local % ndev
+    n, so, K, W = args.n, args.so, args.steps, args.warmup
+    shape = (n * world, n, n)
+    nt_total = K + W + 8
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
+                                                   steps=nt_total))
+    slab = D.slab_bounds(shape[0], world, rank) if world > 1 else None
+    m, damp = prob.m_data(), prob.damp_data()
+    op = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
+    if world > 1:
+        D.exchange_and_link(op, rank, world)
+    lo, hi = op.slab
+    h = so // 2
+    pts_local = (min(hi, n * world - h) - max(lo, h)) * (n - so) * (n - so)
+    pts_total = allsum(pts_local, world)
+    # warm-up
+    op.apply(W, 0)
+    barrier(world)
+    torch.cuda.synchronize(device)
+    clk = Clocks(device) if rank == 0 else None
+    if clk:
+        clk.start()
+    barrier(world)
+    torch.cuda.synchronize(device)
+    op.apply_async(K, W)
+    op.collect(K)
+    torch.cuda.synchronize(device)
+    barrier(world)
+    st = op.stats()
+    clocks = clk.stop() if clk else None
+    dev_s = allmax(st.device_ms * 1e-3, world)
+    value = pts_total * K / dev_s / 1e9
+    launches = int(st.kernel_launches)
+    stencil_launches = K  # one fused stencil launch per time step
+    mean_launch_s = st.device_ms * 1e-3 / stencil_launches
+    hbm, peak_kind = peaks()
+    achieved = BYTES_PER_POINT * pts_local * (K / stencil_launches) / mean_launch_s / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": traffic_from_profiles(so),
+            "peak_kind": peak_kind, "kernel": "k_tma (factorised 2.5D TMA stencil)",
+            "bytes_per_point": BYTES_PER_POINT}
+    # ---- sweep over the other space orders (device-resident, same protocol) ----
+    sweep = {}
+    if not args.no_sweep:
+        for s2 in (4, 8, 12, 16):
+            if s2 == so:
+                sweep[f"so{s2}"] = {"gpts": round(value, 2), "frac": roof["frac"]}
+                continue
+            p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
+                                                         space_order=s2, steps=args.sweep_steps + 16))
+            o2 = P.Operator(p2, form="factorised", device=device, slab=slab, m=m, damp=damp)
+            if world > 1:
+                D.exchange_and_link(o2, rank, world)
+            o2.apply(5, 0)
+            barrier(world)
+            torch.cuda.synchronize(device)
+            o2.apply_async(args.sweep_steps, 5)
+            o2.collect(args.sweep_steps)
+            barrier(world)
+            t2 = allmax(o2.stats().device_ms * 1e-3, world)
+            hh = s2 // 2
+            pl = (min(hi, n * world - hh) - max(lo, hh)) * (n - s2) * (n - s2)
+            g2 = allsum(pl, world) * args.sweep_steps / t2 / 1e9
+            sweep[f"so{s2}"] = {"gpts": round(g2, 2),
+                                "frac": round(BYTES_PER_POINT * g2 / world / hbm, 4),
+                                "gflops": round(g2 * FLOPS_AGGRESSIVE[s2], 1)}
+            o2.close()
+    op.close()
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        init = [pinned(shape) for _ in range(3)]
+        for a in init:
+            a[...] = 0.0
+        out = [pinned(shape) for _ in range(3)]
+        barrier(world)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        o3 = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
+        if world > 1:
+            D.exchange_and_link(o3, rank, world)
+        for l in range(3):
+            o3.set_level(l, init[l])
+        r = o3.apply(K, 0)
+        for l in range(3):
+            o3.get_level(l, out[l])
+        barrier(world)
+        t1 = time.perf_counter()
+        o3.close()
+        e2e_s = allmax(t1 - t0, world)
+        planes = hi - lo
+        h2d = (2 + 3) * planes * n * n * 4 + 4 * prob.source.wavelet.size
+        d2h = 3 * planes * n * n * 4 + 4 * K
+        e2e = {"value": round(pts_total * K / e2e_s / 1e9, 2), "unit": "GPts/s",
+               "h2d_bytes_per_step": int(allsum(h2d, world) / K),
+               "d2h_bytes_per_step": int(allsum(d2h, world) / K),
+               "seconds": round(e2e_s, 4),
+               "includes": "handle create (H2D m, damp, wavelet) + H2D 3 levels (pinned) + K steps + "
+                           "D2H 3 levels + per-step max|u|"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(n, so, args.cpu_steps)
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GPts/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": round(dev_s * 1e3 / K, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"3D acoustic isotropic FD, {n}^3 per GPU (global {shape[0]}x{n}x{n}), "
+                                   f"SO {so}, factorised form, c=1500 m/s, h=10 m, dt=cfl_dt, Ricker 10 Hz",
+                       "grid": list(shape), "space_order": so, "time_steps_timed": K,
+                       "points_per_step": int(pts_total),
+                       "l2": "inputs larger than L2 (20 B/pt x 15.3M pts = 305 MB/step > 126 MB)",
+                       "parallelism": f"z-slab x{world} (reference dim 0), peer-memory halo exchange"},
+            "gflops": round(value * FLOPS_AGGRESSIVE[so], 1),
+            "roofline": roof, "sweep": sweep, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(res), flush=True)
+
+
+def cpu_baseline(n, so, steps):
+    """The reference's own exec::run (oracle/_ref, basic IET, all host threads) on a bounded
+    sample of the workload; falls back to the C restatement (oracle/port) if _ref is absent."""
+    from oracle import bindings as O
+    cfg = O.OracleConfig(shape=(n, n, n), space_order=so, steps=steps)
+    try:
+        if O.ref_available():
+            r = O.ref_run(cfg, threads=0)
+            kind, cores = "reference", O.omp_threads("ref")
+        else:
+            r = O.port_run(cfg, threads=0)
+            kind, cores = "port", O.omp_threads("port")
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+    gp = r["point_updates"] / r["wall_seconds"] / 1e9
+    return {"value": round(gp, 6), "unit": "GPts/s", "cores": cores, "kind": kind,
+            "sample": f"{n}^3 SO {so}, {steps} time steps of exec::run (basic DSE), "
+                      f"RunResult.point_updates / wall_seconds ({r['wall_seconds']:.2f} s)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU path on this arm's config (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import bindings as O
+    n, so = args.n, args.so
+    shape = (n * world, n, n)
+    steps = max(1, min(args.steps, args.ref_steps))
+    cfg = O.OracleConfig(shape=shape, space_order=so, steps=steps)
+    use_ref = O.ref_available()
+    fn = O.ref_run if use_ref else O.port_run
+    r = fn(cfg, threads=0)
+    gp = r["point_updates"] / r["wall_seconds"] / 1e9
+    kind = "reference" if use_ref else "port"
+    cores = O.omp_threads("ref" if use_ref else "port")
+    res = {
+        "metric": METRIC, "value": round(gp, 6), "unit": "GPts/s", "n_gpus": world, "steps": steps,
+        "warmup": 0, "ms_per_step": round(r["wall_seconds"] * 1e3 / steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp64-compute/fp32-storage", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"3D acoustic isotropic FD, global {shape[0]}x{n}x{n}, SO {so}, basic DSE "
+                               f"(exec::run, OpenMP)", "grid": list(shape), "space_order": so},
+        "cpu_baseline": {"value": round(gp, 6), "unit": "GPts/s", "cores": cores, "kind": kind,
+                         "sample": f"{steps} time steps of the full grid (bounded sample; the K requested "
+                                   f"steps would take {args.steps * r['wall_seconds'] / steps:.0f} s)"},
+        "e2e": {"value": round(gp, 6), "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--so", type=int, default=8)
+    ap.add_argument("--sweep-steps", type=int, default=300)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--ref-steps", type=int, default=3)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("warmup must be >= 3")
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -122,10 +122,22 @@ __global__ void k_receivers(const float* __restrict__ un, const long long* __res
 
 // Halo-exchange ordering: spin until every linked neighbour has completed at least
 // `need` steps (counters live in this handle's memory and are written by the neighbours).
+// Bounded: after `timeout_ns` the kernel records an error instead of hanging the device.
 __global__ void k_wait_flags(const volatile unsigned long long* flags, int mask,
-                             unsigned long long need) {
+                             unsigned long long need, unsigned long long timeout_ns,
+                             unsigned* err) {
     if (threadIdx.x < 2 && ((mask >> threadIdx.x) & 1)) {
-        while (flags[threadIdx.x] < need) __nanosleep(64);
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (flags[threadIdx.x] < need) {
+            __nanosleep(100);
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) {
+                atomicExch(err, 1u);
+                break;
+            }
+        }
     }
     __syncthreads();
     __threadfence_system();
@@ -160,8 +172,8 @@ cudaError_t launch_receivers(const float* un, const long long* idx, int n, float
 }
 
 cudaError_t launch_wait_flags(const unsigned long long* flags, int mask,
-                              unsigned long long need, cudaStream_t s) {
-    k_wait_flags<<<1, 32, 0, s>>>(flags, mask, need);
+                              unsigned long long need, unsigned* err, cudaStream_t s) {
+    k_wait_flags<<<1, 32, 0, s>>>(flags, mask, need, 20000000000ull, err);
     return cudaGetLastError();
 }
 

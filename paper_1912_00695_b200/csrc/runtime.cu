@@ -77,6 +77,7 @@ struct swb_handle {
     unsigned char* d_dflag = nullptr;
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
+    unsigned* d_err = nullptr;                // halo-exchange timeout flag
     unsigned long long* lo_remote = nullptr; // lower neighbour's d_flags[1]
     unsigned long long* hi_remote = nullptr; // upper neighbour's d_flags[0]
     void* ipc_lo_u = nullptr;
@@ -177,7 +178,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
         const bool linked = h->lo_remote || h->hi_remote;
         if (linked) {
             const int mask = (h->lo_remote ? 1 : 0) | (h->hi_remote ? 2 : 0);
-            SWB_CUDA(launch_wait_flags(h->d_flags, mask, h->steps_done + i, h->stream));
+            SWB_CUDA(launch_wait_flags(h->d_flags, mask, h->steps_done + i, h->d_err, h->stream));
             ++h->launches;
         }
         Ctl c = h->ctl;
@@ -328,6 +329,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     SWB_CUDA_C(cudaMalloc(&h->d_ring, 3 * sizeof(unsigned)));
     SWB_CUDA_C(cudaMalloc(&h->d_flags, 2 * sizeof(unsigned long long)));
     SWB_CUDA_C(cudaMemsetAsync(h->d_flags, 0, 2 * sizeof(unsigned long long), h->stream));
+    SWB_CUDA_C(cudaMalloc(&h->d_err, sizeof(unsigned)));
+    SWB_CUDA_C(cudaMemsetAsync(h->d_err, 0, sizeof(unsigned), h->stream));
 
     // m / damp for every local plane (ghost planes included; they are never read).
     const size_t row = sizeof(float) * h->n2;
@@ -498,6 +501,12 @@ int swb_collect(swb_handle* h, float* step_max_abs, int32_t* first_bad_step, flo
             static_cast<uint64_t>(h->geo.y1 - h->geo.y0) * static_cast<uint64_t>(h->geo.z1 - h->geo.z0) +
         (h->ctl.has_src ? 1u : 0u);
     h->stats.point_updates += per_step * static_cast<uint64_t>(nt);
+    unsigned herr = 0;
+    SWB_CUDA(cudaMemcpy(&herr, h->d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    if (herr) {
+        cudaMemset(h->d_err, 0, sizeof herr);
+        return fail(SWB_ECUDA, "halo exchange timed out waiting for a neighbour slab");
+    }
     std::vector<unsigned> smax(static_cast<size_t>(nt)), ring(3);
     if (nt > 0)
         SWB_CUDA(cudaMemcpy(smax.data(), h->d_smax, sizeof(unsigned) * nt, cudaMemcpyDeviceToHost));
@@ -561,7 +570,7 @@ int swb_destroy(swb_handle* h) {
                     static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
                     static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
-                    static_cast<void*>(h->d_dflag)})
+                    static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err)})
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);

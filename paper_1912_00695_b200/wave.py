@@ -318,7 +318,8 @@ class Operator:
     def __init__(self, problem: WaveProblem, dse: DseLevel = DseLevel.aggressive, *,
                  form: Optional[str] = None, receivers: Optional[np.ndarray] = None,
                  device: int = 0, time_block: int = 1,
-                 slab: Optional[Tuple[int, int]] = None):
+                 slab: Optional[Tuple[int, int]] = None,
+                 m: Optional[np.ndarray] = None, damp: Optional[np.ndarray] = None):
         self.problem = problem
         self.form = form or form_for(dse)
         if self.form not in _FORMS:
@@ -330,8 +331,12 @@ class Operator:
             p.spacing[d] = np.float32(problem.spacing[d])
         p.space_order = problem.space_order
         p.dt = float(problem.dt)
-        m = np.ascontiguousarray(problem.m_data(), np.float32)
-        damp = np.ascontiguousarray(problem.damp_data(), np.float32)
+        # m / damp may be passed precomputed (e.g. pinned host buffers); they must equal
+        # problem.m_data() / problem.damp_data().
+        m = np.ascontiguousarray(problem.m_data() if m is None else m, np.float32)
+        damp = np.ascontiguousarray(problem.damp_data() if damp is None else damp, np.float32)
+        if m.size != problem.cell_count() or damp.size != problem.cell_count():
+            raise ValueError("m/damp size does not match the grid")
         w = rounded_weights(problem.space_order)
         self._keep += [m, damp, w]
         p.m = N.fptr(m)
