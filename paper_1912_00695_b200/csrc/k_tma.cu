@@ -26,145 +26,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 
-#include "k_common.cuh"
-#include "kernels.h"
+#include "k_tma_common.cuh"
 
 namespace swb {
 namespace {
+using namespace tma;
 
-constexpr int kT2 = 64;  // output cols per tile (16 lanes x float4)
-
-struct Maps {
-    CUtensorMap u[3];     // halo box (W2, T1+2H, 1)
-    CUtensorMap a[3];     // aux box (64, T1, 1) over the u levels (for u[t-1])
-    CUtensorMap m;        // aux box over m
-    CUtensorMap damp;     // aux box over damp
-};
-
-struct Sched {
-    int nyt, nzt, ncol;   // column tiles
-    int np;               // planes to update per column
-    int nchunk;           // dim-0 chunks per column (work items = ncol * nchunk)
-    int y0, y1, z0, z1, zs, x0;
-    const unsigned char* dflag;  // [ncol][np]: damp tile non-zero (null = always load damp)
-};
-
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int c0, int c1,
-                                          int c2, unsigned bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load3_hint(unsigned dst, const CUtensorMap* map, int c0, int c1,
-                                               int c2, unsigned bar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ float4 lds4(unsigned addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ float comp(const float4& v, int e) {
-    return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
-}
-__device__ __forceinline__ void set_comp(float4& v, int e, float x) {
-    if (e == 0) v.x = x;
-    else if (e == 1) v.y = x;
-    else if (e == 2) v.z = x;
-    else v.w = x;
-}
-
-template <int H, int R1, int T1>
-struct Cfg {
-    static constexpr int A = (H + 3) / 4 * 4;         // dim-2 halo rounded to float4
-    static constexpr int W2 = kT2 + 2 * A;             // smem row length (floats)
-    static constexpr int ROWS = T1 + 2 * H;            // smem rows per plane
-    static constexpr int UPLANE = (ROWS * W2 * 4 + 127) / 128 * 128;
-    static constexpr int ATILE = T1 * kT2 * 4;         // one aux tile (bytes)
-    static constexpr int NCW = (T1 / R1) * 16 / 32;    // consumer warps
-    static constexpr int NTHREADS = 32 * (NCW + 1);
-    static constexpr int NQ = 2 * H + 1;               // queue depth
-};
-
-// ---- packed FP32x2 arithmetic (FADD2 / FFMA2 / FMUL2 on sm_100a) --------------------
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    return __ffma2_rn(b, make_float2(-1.f, -1.f), a);  // a - b, one rounding
-}
-__device__ __forceinline__ float2 splat(float v) { return make_float2(v, v); }
-__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-// n / d with one Newton step on MUFU.RCP: error <= 1 ulp of the quotient (the quotient is the
-// per-step increment, ~0.1 |u|, so this is ~0.1 ulp of u; see DESIGN.md numerics).
-__device__ __forceinline__ float2 div2(float2 n, float2 d) {
-    const float2 r = make_float2(rcp_approx(d.x), rcp_approx(d.y));
-    const float2 q = mul2(n, r);
-    const float2 e = fma2(make_float2(-d.x, -d.y), q, n);
-    return fma2(e, r, q);
-}
-
-// Advance a ring position (stage, phase) by one.
-template <int S>
-__device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {
-    if (++st == S) {
-        st = 0;
-        ph ^= 1u;
-    }
-}
-
-// Per-item state shared by the consumer's per-plane steps.
-struct Item {
-    int xa, xb, dir, q0, nq, yt, zc;
-    bool zfull, rows_ok;
-    long long gcol;
-};
-
-// One arrival step of a consumer thread: take plane q's centre values into queue slot U,
-// and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
-// (U - H) mod NQ.  All queue indices are compile-time.
 template <int H, int R1, int T1, int SU, int SA, int U>
 __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][2 * H + 1], int j, const Item& it,
                                               const float* ucol, const float* acol,
@@ -394,47 +265,55 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     unsigned mine = 0u;
 
     if (warp == 0) {
-        // ===== TMA producer (one elected lane) =====
-        if (lane == 0) {
+        // ===== TMA producers: lane 0 feeds the u ring, lane 1 the aux ring, each limited
+        // only by its own ring (independent progress of diverged lanes, sm_70+) =====
+        if (lane < 2) {
             const CUtensorMap* mu = &maps.u[lt];
             const CUtensorMap* ma = &maps.a[lp];
-            prefetch_map(mu);
-            prefetch_map(ma);
-            prefetch_map(&maps.m);
-            prefetch_map(&maps.damp);
+            if (lane == 0) {
+                prefetch_map(mu);
+            } else {
+                prefetch_map(ma);
+                prefetch_map(&maps.m);
+                prefetch_map(&maps.damp);
+            }
             uint64_t pol_first;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-            constexpr int DA = SA - 1 < 2 ? SA - 1 : 2;  // aux prefetch distance (planes)
-            unsigned su = 0, pu = 0, sa = 0, pa_ = 0;
+            unsigned st = 0, ph = 0;
             for (int item = blockIdx.x; item < nitems; item += G) {
                 const int col = item % sc.ncol, chunk = item / sc.ncol;
                 const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
                 const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
                 const int dir = (chunk & 1) ? 1 : -1;   // even chunks descend, odd ascend
-                const int q0 = dir > 0 ? xa - H : xb - 1 + H;
-                const int nq = xb - xa + 2 * H;
                 const int yt = sc.y0 + (col / sc.nzt) * T1;
                 const int zt = sc.zs + (col % sc.nzt) * kT2;
-                const unsigned char* dfl = sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
-                for (int j = 0; j < nq; ++j) {
-                    const int q = q0 + dir * j;
-                    mbar_wait(empty_u + 8 * su, pu ^ 1u);
-                    mbar_expect_tx(full_u + 8 * su, C::ROWS * C::W2 * 4);
-                    tma_load3(uring_s + su * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * su);
-                    ring_next<SU>(su, pu);
-                    const int p = q - dir * (H - DA);
-                    if (p >= xa && p < xb) {
-                        mbar_wait(empty_a + 8 * sa, pa_ ^ 1u);
+                if (lane == 0) {
+                    const int q0 = dir > 0 ? xa - H : xb - 1 + H;
+                    const int nq = xb - xa + 2 * H;
+                    for (int j = 0; j < nq; ++j) {
+                        const int q = q0 + dir * j;
+                        mbar_wait(empty_u + 8 * st, ph ^ 1u);
+                        mbar_expect_tx(full_u + 8 * st, C::ROWS * C::W2 * 4);
+                        tma_load3(uring_s + st * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * st);
+                        ring_next<SU>(st, ph);
+                    }
+                } else {
+                    const unsigned char* dfl =
+                        sc.dflag ? sc.dflag + static_cast<long long>(col) * sc.np - sc.x0 : nullptr;
+                    const int p0 = dir > 0 ? xa : xb - 1;
+                    for (int j = 0; j < xb - xa; ++j) {
+                        const int p = p0 + dir * j;
+                        mbar_wait(empty_a + 8 * st, ph ^ 1u);
                         const unsigned need_damp = (!dfl || dfl[p]) ? 1u : 0u;
-                        aflag[sa] = need_damp;  // published by the arrive below (release)
-                        mbar_expect_tx(full_a + 8 * sa, (need_damp ? 3 : 2) * C::ATILE);
-                        const unsigned dst = aring_s + sa * 3 * C::ATILE;
-                        tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * sa, pol_first);
-                        tma_load3_hint(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * sa, pol_first);
+                        aflag[st] = need_damp;  // published by the arrive below (release)
+                        mbar_expect_tx(full_a + 8 * st, (need_damp ? 3 : 2) * C::ATILE);
+                        const unsigned dst = aring_s + st * 3 * C::ATILE;
+                        tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * st, pol_first);
+                        tma_load3_hint(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * st, pol_first);
                         if (need_damp)
-                            tma_load3_hint(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * sa,
+                            tma_load3_hint(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * st,
                                            pol_first);
-                        ring_next<SA>(sa, pa_);
+                        ring_next<SA>(st, ph);
                     }
                 }
             }
@@ -502,14 +381,14 @@ size_t smem_bytes() {
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
 #define SWB_TMA_VARIANTS(X)         \
-    X(1, 2, 28, 4, 3)               \
-    X(2, 2, 28, 5, 3)               \
-    X(3, 2, 28, 6, 3)               \
-    X(4, 2, 28, 7, 3)               \
-    X(5, 2, 28, 8, 3)               \
-    X(6, 2, 28, 9, 3)               \
-    X(7, 2, 28, 10, 2)              \
-    X(8, 2, 28, 11, 2)
+    X(1, 2, 28, 5, 4)               \
+    X(2, 2, 28, 6, 4)               \
+    X(3, 2, 28, 7, 4)               \
+    X(4, 2, 28, 8, 4)               \
+    X(5, 2, 28, 9, 4)               \
+    X(6, 2, 28, 10, 3)               \
+    X(7, 2, 28, 11, 3)              \
+    X(8, 2, 28, 11, 3)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
 
@@ -561,21 +440,42 @@ bool encode(CUtensorMap* map, const float* base, int n2, int n1, int nl0, int P2
 
 }  // namespace
 
+bool sq_variant(int H, int* T1, int* threads, int* smem, const void** fn);
+cudaError_t launch_sq(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K, const Ctl& c,
+                      const Peer& p, const void* sched, cudaStream_t s);
+
+// Kernel choice: the register-queue variant (this file) by default -- measured faster than
+// the smem-queue variant (k_sq.cu) at every SO (equal at SO 4/8 on 256^3, +40% at 512^3 SO 8,
+// +30% at SO 16); SWB_KERNEL=sq selects the smem-queue variant.
 TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     TmaPlan p{};
     p.ok = 0;
     p.H = H;
-    const Variant* v = find_variant(H);
-    if (!v) return p;
-    p.T1 = v->T1;
+    const char* env = std::getenv("SWB_KERNEL");
+    const bool want_rq = !(env && std::strcmp(env, "sq") == 0);
+    int T1 = 0, threads = 0, smem = 0;
+    const void* fn = nullptr;
+    if (!want_rq && sq_variant(H, &T1, &threads, &smem, &fn)) {
+        p.kind = 1;
+        p.variant = 2000 + H;
+    } else {
+        const Variant* v = find_variant(H);
+        if (!v) return p;
+        T1 = v->T1;
+        threads = v->threads;
+        smem = static_cast<int>(v->smem);
+        fn = reinterpret_cast<const void*>(v->fn);
+        p.kind = 0;
+        p.variant = 1000 + H;
+    }
+    p.T1 = T1;
     p.T2 = kT2;
     p.A = (H + 3) / 4 * 4;
-    p.stages = v->SU;
-    p.threads = v->threads;
-    p.smem_bytes = static_cast<int>(v->smem);
+    p.threads = threads;
+    p.smem_bytes = smem;
     const int zs = g.z0 & ~3;
     p.zs = zs;
-    p.tiles_y = ceil_div(g.y1 - g.y0, v->T1);
+    p.tiles_y = ceil_div(g.y1 - g.y0, T1);
     p.tiles_z = ceil_div(g.z1 - zs, kT2);
     p.columns = p.tiles_y * p.tiles_z;
     const int np = g.x1 - g.x0;
@@ -589,9 +489,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     nchunk = std::min(nchunk, std::max(1, np / std::max(2, 2 * H)));
     p.nchunk = nchunk;
     p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * nchunk));
-    p.variant = 1000 + H;
-    if (cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(v->smem)) != cudaSuccess) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return p;
     }
@@ -644,7 +542,7 @@ void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp, int n1
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s) {
     const Variant* v = find_variant(plan.H);
-    if (!v || !plan.ok) return cudaErrorInvalidValue;
+    if (!plan.ok || (plan.kind == 0 && !v)) return cudaErrorInvalidValue;
     Sched sc;
     sc.nyt = plan.tiles_y;
     sc.nzt = plan.tiles_z;
@@ -658,6 +556,7 @@ cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, cons
     sc.z1 = g.z1;
     sc.zs = plan.zs;
     sc.x0 = g.x0;
+    if (plan.kind == 1) return launch_sq(plan, maps, g, K, c, p, &sc, s);
     v->fn<<<plan.grid, v->threads, v->smem, s>>>(*static_cast<const Maps*>(maps), g, K, c, p, sc);
     return cudaGetLastError();
 }

@@ -1,0 +1,147 @@
+// Shared device helpers of the TMA stencil kernels (k_tma.cu, k_sq.cu): mbarrier/TMA PTX
+// wrappers, packed FP32x2 arithmetic, tensor-map bundle, work schedule.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "k_common.cuh"
+#include "kernels.h"
+
+namespace swb {
+namespace tma {
+
+constexpr int kT2 = 64;  // output cols per tile (16 lanes x float4)
+
+struct Maps {
+    CUtensorMap u[3];     // halo box (W2, T1+2H, 1)
+    CUtensorMap a[3];     // aux box (64, T1, 1) over the u levels (for u[t-1])
+    CUtensorMap m;        // aux box over m
+    CUtensorMap damp;     // aux box over damp
+};
+
+struct Sched {
+    int nyt, nzt, ncol;   // column tiles
+    int np;               // planes to update per column
+    int nchunk;           // dim-0 chunks per column (work items = ncol * nchunk)
+    int y0, y1, z0, z1, zs, x0;
+    const unsigned char* dflag;  // [ncol][np]: damp tile non-zero (null = always load damp)
+};
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                          int c2, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load3_hint(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                               int c2, unsigned bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ float4 lds4(unsigned addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float comp(const float4& v, int e) {
+    return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void set_comp(float4& v, int e, float x) {
+    if (e == 0) v.x = x;
+    else if (e == 1) v.y = x;
+    else if (e == 2) v.z = x;
+    else v.w = x;
+}
+
+template <int H, int R1, int T1>
+struct Cfg {
+    static constexpr int A = (H + 3) / 4 * 4;         // dim-2 halo rounded to float4
+    static constexpr int W2 = kT2 + 2 * A;             // smem row length (floats)
+    static constexpr int ROWS = T1 + 2 * H;            // smem rows per plane
+    static constexpr int UPLANE = (ROWS * W2 * 4 + 127) / 128 * 128;
+    static constexpr int ATILE = T1 * kT2 * 4;         // one aux tile (bytes)
+    static constexpr int NCW = (T1 / R1) * 16 / 32;    // consumer warps
+    static constexpr int NTHREADS = 32 * (NCW + 1);
+    static constexpr int NQ = 2 * H + 1;               // queue depth
+};
+
+// ---- packed FP32x2 arithmetic (FADD2 / FFMA2 / FMUL2 on sm_100a) --------------------
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    return __ffma2_rn(b, make_float2(-1.f, -1.f), a);  // a - b, one rounding
+}
+__device__ __forceinline__ float2 splat(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// n / d with one Newton step on MUFU.RCP: error <= 1 ulp of the quotient (the quotient is the
+// per-step increment, ~0.1 |u|, so this is ~0.1 ulp of u; see DESIGN.md numerics).
+__device__ __forceinline__ float2 div2(float2 n, float2 d) {
+    const float2 r = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+    const float2 q = mul2(n, r);
+    const float2 e = fma2(make_float2(-d.x, -d.y), q, n);
+    return fma2(e, r, q);
+}
+
+// Advance a ring position (stage, phase) by one.
+template <int S>
+__device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {
+    if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+    }
+}
+
+// Per-item state shared by the consumer's per-plane steps.
+struct Item {
+    int xa, xb, dir, q0, nq, yt, zc;
+    bool zfull, rows_ok;
+    long long gcol;
+};
+
+// One arrival step of a consumer thread: take plane q's centre values into queue slot U,
+// and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
+// (U - H) mod NQ.  All queue indices are compile-time.
+}  // namespace tma
+}  // namespace swb

@@ -26,6 +26,7 @@ struct TmaPlan {
     int nchunk;           // dim-0 chunks per column
     const unsigned char* dflag;  // device [columns][planes] damp-tile-nonzero flags (or null)
     int variant;
+    int kind;             // 0: register-queue kernel (k_tma.cu), 1: smem-queue kernel (k_sq.cu)
 };
 // Host-side damp tile flags for a plan: flags[col * np + (x - x0)] = any damp != 0 in the tile.
 void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_local, int n1, int n2,

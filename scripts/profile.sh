@@ -1,0 +1,10 @@
+#!/bin/bash
+# ncu evidence for the stencil kernels (run under gpurun; one GPU).
+set -x
+mkdir -p gpurun_out
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > gpurun_out/launches_bench.log 2>&1
+for so in ${SOS:-4 8 12 16}; do
+  ncu --set full --clock-control none --import-source on -k regex:k_tma -s 6 -c 1 \
+      -o gpurun_out/tma_so$so python scripts/probe_perf.py factorised $so 256 8 > gpurun_out/ncu_so$so.log 2>&1
+done

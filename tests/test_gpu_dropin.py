@@ -1,0 +1,43 @@
+"""The reference tree rebuilt with integration/executor_b200.cpp instead of
+src/executor.cpp (oracle/_ref/dropin_run, built by `make -C oracle dropin` where
+/root/reference exists): the reference's own call sequence
+make_wave_problem -> wave_equations -> lower -> optimize_all -> build_iet -> exec::run
+now runs on the B200 kernels.  basic IET: bit-exact with the oracle; aggressive IET:
+<= 1e-5 relative L2 (the sign-corrected factorised form)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import bindings as O
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "oracle", "_ref", "dropin_run")
+
+
+def run_dropin(dse, shape, so, steps, damp, tmp_path):
+    out = tmp_path / f"{dse}.bin"
+    p = subprocess.run([EXE, dse, *map(str, shape), str(so), str(steps), str(damp), str(out)],
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    raw = out.read_bytes()
+    fl = int(np.frombuffer(raw[:4], np.int32)[0])
+    pu = int(np.frombuffer(raw[4:12], np.uint64)[0])
+    smax = np.frombuffer(raw[12:12 + 4 * steps], np.float32)
+    levels = np.frombuffer(raw[12 + 4 * steps:], np.float32).reshape((3,) + tuple(shape))
+    return fl, pu, smax, levels
+
+
+@pytest.mark.skipif(not os.path.exists(EXE), reason="drop-in binary not built (needs /root/reference)")
+@pytest.mark.parametrize("so,damp", [(2, 0.0), (8, 0.05), (16, 0.0)])
+def test_reference_api_runs_on_b200(so, damp, tmp_path):
+    shape, steps = (so + 14, so + 15, so + 16), 11
+    ref = O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=steps, damp_max=damp, damp_width=4))
+    fl, pu, smax, lv = run_dropin("basic", shape, so, steps, damp, tmp_path)
+    assert fl == ref["final_level"] and pu == ref["point_updates"]
+    assert np.array_equal(lv, ref["levels"]) and np.array_equal(smax, ref["step_max_abs"])
+    fl, pu, smax, lv = run_dropin("aggressive", shape, so, steps, damp, tmp_path)
+    err = np.linalg.norm(lv[fl] - ref["levels"][fl]) / np.linalg.norm(ref["levels"][fl])
+    assert err <= 1e-5
