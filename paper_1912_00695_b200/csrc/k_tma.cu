@@ -26,7 +26,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <cstdint>
 #include <cstring>
 
@@ -388,7 +390,15 @@ size_t smem_bytes() {
     X(5, 2, 28, 9, 4)               \
     X(6, 2, 28, 10, 3)               \
     X(7, 2, 28, 11, 3)              \
-    X(8, 2, 28, 11, 3)
+    X(8, 2, 28, 11, 3)              \
+    X(1, 1, 30, 5, 4)               \
+    X(2, 1, 30, 6, 4)               \
+    X(3, 1, 30, 7, 4)               \
+    X(4, 1, 30, 8, 4)               \
+    X(5, 1, 30, 9, 4)               \
+    X(6, 1, 30, 10, 3)              \
+    X(7, 1, 22, 11, 3)              \
+    X(8, 1, 22, 11, 3)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
 
@@ -402,8 +412,20 @@ struct Variant {
 #define SWB_VARIANT_ENTRY(h, r1, t1, su, sa) \
     {h, r1, t1, su, sa, k_tma<h, r1, t1, su, sa>, smem_bytes<h, r1, t1, su, sa>(), Cfg<h, r1, t1>::NTHREADS},
 
+// Rows per consumer thread: R1 = 1 doubles the consumer warps per SM (more latency hiding)
+// at the cost of re-reading the y-neighbour rows per row; SWB_R1=1|2 overrides the default.
+int preferred_r1(int H) {
+    const char* env = std::getenv("SWB_R1");
+    if (env && (env[0] == '1' || env[0] == '2')) return env[0] - '0';
+    (void)H;
+    return 1;
+}
+
 const Variant* find_variant(int H) {
     static const Variant table[] = {SWB_TMA_VARIANTS(SWB_VARIANT_ENTRY)};
+    const int r1 = preferred_r1(H);
+    for (const auto& v : table)
+        if (v.H == H && v.R1 == r1) return &v;
     for (const auto& v : table)
         if (v.H == H) return &v;
     return nullptr;
@@ -466,7 +488,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         smem = static_cast<int>(v->smem);
         fn = reinterpret_cast<const void*>(v->fn);
         p.kind = 0;
-        p.variant = 1000 + H;
+        p.variant = 1000 + 100 * (v->R1 - 1) + H;
     }
     p.T1 = T1;
     p.T2 = kT2;
@@ -484,11 +506,23 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // Work items: column tiles x dim-0 chunks.  Chunk boundaries line up across columns and
     // alternate direction (even chunks descend, odd ascend), so CTAs meeting at a chunk
     // boundary read the shared planes at the same time (L2 hits), and neighbouring columns
-    // stream the same planes concurrently (halo re-reads hit L2).
-    int nchunk = std::max(1, num_sms / p.columns);
-    nchunk = std::min(nchunk, std::max(1, np / std::max(2, 2 * H)));
-    p.nchunk = nchunk;
-    p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * nchunk));
+    // stream the same planes concurrently (halo re-reads hit L2).  The chunk count minimises
+    // the estimated makespan: rounds of items over the persistent CTAs x (chunk length +
+    // warm-up of 2H planes, which cost about half an output plane each).
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nc = 1; nc <= 32 && nc <= np; ++nc) {
+        const long long items = static_cast<long long>(p.columns) * nc;
+        const long long rounds = (items + num_sms - 1) / num_sms;
+        const double len = static_cast<double>(np) / nc;
+        const double cost = static_cast<double>(rounds) * (std::ceil(len) + 0.5 * 2 * H);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = nc;
+        }
+    }
+    p.nchunk = best;
+    p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * best));
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return p;
