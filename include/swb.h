@@ -159,6 +159,11 @@ int swb_damp_data(const int32_t* shape, float damp_max, int damp_width, float* o
 /* Version / build info string. */
 const char* swb_version(void);
 
+/* Debug: with SWB_TRACE=1 in the environment at swb_create, copy the per-CTA globaltimer
+ * stamps [cta][start, warm-up done, compute done, exit] of the last stencil launch.
+ * Returns the number of CTAs of that launch (or a negative error). */
+int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

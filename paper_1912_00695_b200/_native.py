@@ -68,6 +68,7 @@ def _load() -> C.CDLL:
         "swb_m_data": (C.c_int, [fp, C.c_size_t, fp]),
         "swb_damp_data": (C.c_int, [P(C.c_int32), C.c_float, C.c_int, fp]),
         "swb_version": (C.c_char_p, []),
+        "swb_debug_trace": (C.c_int, [h, P(C.c_uint64), C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -82,7 +83,8 @@ lib = _load()
 EXPORTED = ["swb_create", "swb_set_level", "swb_get_level", "swb_apply", "swb_apply_async",
             "swb_collect", "swb_stream", "swb_get_stats", "swb_destroy", "swb_last_error",
             "swb_export_ghosts", "swb_link_neighbours", "swb_link_local", "swb_fd_weights",
-            "swb_cfl_dt", "swb_ricker_wavelet", "swb_m_data", "swb_damp_data", "swb_version"]
+            "swb_cfl_dt", "swb_ricker_wavelet", "swb_m_data", "swb_damp_data", "swb_version",
+            "swb_debug_trace"]
 
 
 def last_error() -> str:

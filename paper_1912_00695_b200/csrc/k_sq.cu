@@ -159,13 +159,12 @@ __device__ __forceinline__ void sq_output(const float* ring, unsigned sc, const 
     const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
     const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
     const bool src_plane = c.has_src && p == c.src_x;
-    if (it.zfull && it.rows_ok && !(lo_m || hi_m || src_plane)) {
+    if (!(lo_m || hi_m || src_plane)) {
+        // common path: plain stores (rows past the interior are skipped warp-uniformly)
 #pragma unroll
-        for (int i = 0; i < R1; ++i) {
-            *reinterpret_cast<float4*>(un + xoff + static_cast<long long>(i) * g.P2) = out[i];
-            mine = max(mine, max(max(abs_bits(out[i].x), abs_bits(out[i].y)),
-                                 max(abs_bits(out[i].z), abs_bits(out[i].w))));
-        }
+        for (int i = 0; i < R1; ++i)
+            if (it.rows_ok || it.yt + i < g.y1)
+                store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
         return;
     }
 #pragma unroll
@@ -261,6 +260,7 @@ __global__ void __launch_bounds__(SqCfg<H, R1, T1, SU>::NTHREADS, 1)
             const int zt = sc.zs + (col % sc.nzt) * kT2;
             it.zc = zt + 4 * tz;
             it.zfull = it.zc >= sc.z0 && it.zc + 3 < sc.z1;
+            it.zmask = zmask_of(it.zc, sc.z0, sc.z1);
             it.rows_ok = it.yt + R1 - 1 < sc.y1;
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
             // aux loads: per-row in-plane index, clamped into the allocation for masked rows /

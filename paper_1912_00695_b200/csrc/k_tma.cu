@@ -164,14 +164,12 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][2 * H + 1], int j,
     const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
     const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
     const bool src_plane = c.has_src && p == c.src_x;
-    if (it.zfull && it.rows_ok && !(lo_m || hi_m || src_plane)) {
-        // fast path: full float4 rows, no injection, no peer copies
+    if (!(lo_m || hi_m || src_plane)) {
+        // common path: plain stores (rows past the interior are skipped warp-uniformly)
 #pragma unroll
-        for (int i = 0; i < R1; ++i) {
-            *reinterpret_cast<float4*>(un + xoff + static_cast<long long>(i) * g.P2) = out[i];
-            mine = max(mine, max(max(abs_bits(out[i].x), abs_bits(out[i].y)),
-                                 max(abs_bits(out[i].z), abs_bits(out[i].w))));
-        }
+        for (int i = 0; i < R1; ++i)
+            if (it.rows_ok || it.yt + i < g.y1)
+                store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
         return;
     }
 #pragma unroll
@@ -265,6 +263,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     const int G = gridDim.x;
     const int nitems = sc.ncol * sc.nchunk;
     unsigned mine = 0u;
+    if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x] = gtimer();
 
     if (warp == 0) {
         // ===== TMA producers: lane 0 feeds the u ring, lane 1 the aux ring, each limited
@@ -346,9 +345,16 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             const int zt = sc.zs + (col % sc.nzt) * kT2;
             it.zc = zt + 4 * tz;  // first z of this thread's float4
             it.zfull = it.zc >= sc.z0 && it.zc + 3 < sc.z1;
+            it.zmask = zmask_of(it.zc, sc.z0, sc.z1);
             it.rows_ok = it.yt + R1 - 1 < sc.y1;
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
             sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
+            if (c.trace && ct == 0 && item == blockIdx.x) {
+                // time when the first output plane's data is complete (end of warm-up)
+                unsigned s2 = (su + 2 * H) % SU, p2 = pu ^ (((su + 2 * H) / SU) & 1u);
+                mbar_wait(full_u + 8 * s2, p2);
+                c.trace[4 * blockIdx.x + 1] = gtimer();
+            }
             if constexpr (kUnroll) {
 #pragma unroll 1
                 for (int jb = 0; jb < it.nq; jb += NQ)
@@ -371,7 +377,9 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         }
     }
     __syncwarp();
+    if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
     block_max_commit(mine, c.smax + c.slot);
+    if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
 }
 
 template <int H, int R1, int T1, int SU, int SA>

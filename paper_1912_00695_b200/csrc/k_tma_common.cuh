@@ -137,8 +137,35 @@ __device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {
 struct Item {
     int xa, xb, dir, q0, nq, yt, zc;
     bool zfull, rows_ok;
+    unsigned zmask;  // bit e set: element zc+e lies in the updated z range
     long long gcol;
 };
+
+// Per-lane validity mask of the float4 at zc against the updated range [z0, z1).
+__device__ __forceinline__ unsigned zmask_of(int zc, int z0, int z1) {
+    unsigned m = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m |= (zc + e >= z0 && zc + e < z1) ? (1u << e) : 0u;
+    return m;
+}
+
+// Store one output float4 row and fold it into the max|u| bits.  Full lanes take one
+// STG.128; boundary lanes predicated scalar stores; no per-element branches (the partial
+// case only exists on the first/last z tile).
+__device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned zmask, unsigned& mine) {
+    if (zmask == 0xFu) {
+        *reinterpret_cast<float4*>(dst) = o;
+        mine = max(mine, max(max(abs_bits(o.x), abs_bits(o.y)), max(abs_bits(o.z), abs_bits(o.w))));
+    } else if (zmask) {
+        if (zmask & 1u) dst[0] = o.x;
+        if (zmask & 2u) dst[1] = o.y;
+        if (zmask & 4u) dst[2] = o.z;
+        if (zmask & 8u) dst[3] = o.w;
+        const unsigned a = (zmask & 1u) ? abs_bits(o.x) : 0u, b = (zmask & 2u) ? abs_bits(o.y) : 0u;
+        const unsigned cc = (zmask & 4u) ? abs_bits(o.z) : 0u, d = (zmask & 8u) ? abs_bits(o.w) : 0u;
+        mine = max(mine, max(max(a, b), max(cc, d)));
+    }
+}
 
 // One arrival step of a consumer thread: take plane q's centre values into queue slot U,
 // and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -75,6 +76,7 @@ struct swb_handle {
     alignas(128) unsigned char maps[kTmaMapsBytes];
     bool use_tma = false;
     unsigned char* d_dflag = nullptr;
+    unsigned long long* d_trace = nullptr;  // SWB_TRACE: per-CTA timestamps of the last launch
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
     unsigned* d_err = nullptr;                // halo-exchange timeout flag
@@ -423,6 +425,10 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         }
     }
     h->stats.kernel_variant = h->use_tma ? h->plan.variant : 100 + h->form;
+    if (std::getenv("SWB_TRACE") && h->use_tma) {
+        SWB_CUDA_C(cudaMalloc(&h->d_trace, sizeof(unsigned long long) * 4 * 1024));
+        h->ctl.trace = h->d_trace;
+    }
     h->stats.launch_steps = 1;
     compute_peer_ranges(h);
     SWB_CUDA_C(cudaStreamSynchronize(h->stream));
@@ -552,6 +558,15 @@ int swb_apply(swb_handle* h, int step0, int nt, float* step_max_abs, int32_t* fi
 
 void* swb_stream(swb_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
+// Debug (SWB_TRACE=1): copy the per-CTA timestamps of the last stencil launch.
+int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas) {
+    if (!h || !h->d_trace) return fail(SWB_EINVAL, "tracing not enabled (set SWB_TRACE=1)");
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    const int n = std::min(max_ctas, 1024);
+    SWB_CUDA(cudaMemcpy(out, h->d_trace, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
+    return h->plan.grid;
+}
+
 int swb_get_stats(swb_handle* h, swb_stats* out) {
     if (!h || !out) return fail(SWB_EINVAL, "null argument");
     *out = h->stats;
@@ -570,7 +585,8 @@ int swb_destroy(swb_handle* h) {
                     static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
                     static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
-                    static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err)})
+                    static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err),
+                    static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);

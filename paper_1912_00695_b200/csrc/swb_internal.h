@@ -54,7 +54,14 @@ struct Ctl {
     unsigned* smax;         // [nt] per-step max|u| bits (atomicMax over non-negative floats)
     int step;               // absolute step
     int slot;               // index into smax / traces for this step
+    unsigned long long* trace;  // optional per-CTA timestamps [gridDim][4] (SWB_TRACE), or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Peer (halo) exchange: boundary planes written straight into neighbour ghosts.
 struct Peer {
