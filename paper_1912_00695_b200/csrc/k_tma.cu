@@ -38,8 +38,8 @@ namespace swb {
 namespace {
 using namespace tma;
 
-template <int H, int R1, int T1, int SU, int SA, int U>
-__device__ __forceinline__ void consumer_step(float4 (&Q)[R1][2 * H + 1], int j, const Item& it,
+template <int H, int R1, int T1, int SU, int SA, int QN, int U>
+__device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const Item& it,
                                               const float* ucol, const float* acol,
                                               const unsigned* aflag, unsigned full_u,
                                               unsigned empty_u, unsigned full_a, unsigned empty_a,
@@ -49,7 +49,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][2 * H + 1], int j,
                                               const Geo& g, const Coef& K, const Ctl& c,
                                               const Peer& pr) {
     using C = Cfg<H, R1, T1>;
-    constexpr int NQ = 2 * H + 1;
+    constexpr int NQ = QN;  // queue slots; plane j-m sits in slot (U - m) mod QN
     const int q = it.q0 + it.dir * j;
     mbar_wait(full_u + 8 * su, pu);
     const float* plane_q = ucol + su * (C::UPLANE / 4);
@@ -208,7 +208,7 @@ struct Unrolled {
                                                float* hi_peer, const Geo& g, const Coef& K,
                                                const Ctl& c, const Peer& pr) {
         if (jb + U < it.nq) {
-            consumer_step<H, R1, T1, SU, SA, U>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
+            consumer_step<H, R1, T1, SU, SA, 2 * H + 1, U>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
                                                 full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
                                                 lo_peer, hi_peer, g, K, c, pr);
             Unrolled<H, R1, T1, SU, SA, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
@@ -227,7 +227,36 @@ struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
                                                const Peer&) {}
 };
 
-template <int H, int R1, int T1, int SU, int SA>
+template <int H, int R1, int T1, int SU, int SA, int UNR, int U>
+struct ShiftBlock {
+    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + UNR], int jb, const Item& it,
+                                               const float* ucol, const float* acol,
+                                               const unsigned* aflag, unsigned full_u, unsigned empty_u,
+                                               unsigned full_a, unsigned empty_a, unsigned& su,
+                                               unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
+                                               unsigned& mine, float* un, float* lo_peer,
+                                               float* hi_peer, const Geo& g, const Coef& K,
+                                               const Ctl& c, const Peer& pr) {
+        if (jb + U < it.nq) {
+            consumer_step<H, R1, T1, SU, SA, 2 * H + UNR, 2 * H + U>(
+                Q, jb + U, it, ucol, acol, aflag, full_u, empty_u, full_a, empty_a, su, pu, sp, sa, pa_,
+                mine, un, lo_peer, hi_peer, g, K, c, pr);
+            ShiftBlock<H, R1, T1, SU, SA, UNR, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                                                           full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
+                                                           lo_peer, hi_peer, g, K, c, pr);
+        }
+    }
+};
+template <int H, int R1, int T1, int SU, int SA, int UNR>
+struct ShiftBlock<H, R1, T1, SU, SA, UNR, UNR> {
+    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + UNR], int, const Item&, const float*,
+                                               const float*, const unsigned*, unsigned, unsigned, unsigned,
+                                               unsigned, unsigned&, unsigned&, unsigned&, unsigned&,
+                                               unsigned&, unsigned&, float*, float*, float*, const Geo&,
+                                               const Coef&, const Ctl&, const Peer&) {}
+};
+
+template <int H, int R1, int T1, int SU, int SA, int UNR>
 __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     k_tma(const __grid_constant__ Maps maps, Geo g, Coef K, Ctl c, Peer pr, Sched sc) {
     using C = Cfg<H, R1, T1>;
@@ -331,7 +360,8 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         // this thread's column inside a u plane / an aux tile (floats)
         const float* ucol = reinterpret_cast<const float*>(uring) + (r0 + H) * C::W2 + C::A + 4 * tz;
         const float* acol = reinterpret_cast<const float*>(aring) + r0 * kT2 + 4 * tz;
-        float4 Q[R1][NQ];  // register queue along dim 0
+        float4 Q[R1][kUnroll ? NQ : 1];   // rotating register queue (H <= 3)
+        float4 Qs[R1][kUnroll ? 1 : 2 * H + UNR];  // shifting register queue (H >= 4)
         unsigned su = 0, pu = 0, sp = 0, sa = 0, pa_ = 0;
         for (int item = blockIdx.x; item < nitems; item += G) {
             const int col = item % sc.ncol, chunk = item / sc.ncol;
@@ -362,16 +392,18 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                                                         full_a, empty_a, su, pu, sp, sa, pa_, mine,
                                                         un, lo_peer, hi_peer, g, K, c, pr);
             } else {
+                // Partial unroll by UNR with a queue of 2H+UNR slots: plane j-m lives in slot
+                // 2H+u-m inside a block, and the queue shifts down by UNR once per block
+                // (2H/UNR float4 moves per plane instead of 2H).
 #pragma unroll 1
-                for (int j = 0; j < it.nq; ++j) {
+                for (int jb = 0; jb < it.nq; jb += UNR) {
+                    ShiftBlock<H, R1, T1, SU, SA, UNR, 0>::run(Qs, jb, it, ucol, acol, aflag, full_u, empty_u,
+                                                             full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
+                                                             lo_peer, hi_peer, g, K, c, pr);
 #pragma unroll
                     for (int i = 0; i < R1; ++i)
 #pragma unroll
-                        for (int k = 0; k < NQ - 1; ++k) Q[i][k] = Q[i][k + 1];
-                    consumer_step<H, R1, T1, SU, SA, NQ - 1>(Q, j, it, ucol, acol, aflag, full_u,
-                                                             empty_u, full_a, empty_a, su, pu, sp,
-                                                             sa, pa_, mine, un, lo_peer, hi_peer, g,
-                                                             K, c, pr);
+                        for (int k = 0; k < 2 * H; ++k) Qs[i][k] = Qs[i][k + UNR];
                 }
             }
         }
@@ -390,35 +422,37 @@ size_t smem_bytes() {
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
-#define SWB_TMA_VARIANTS(X)         \
-    X(1, 2, 28, 5, 4)               \
-    X(2, 2, 28, 6, 4)               \
-    X(3, 2, 28, 7, 4)               \
-    X(4, 2, 28, 8, 4)               \
-    X(5, 2, 28, 9, 4)               \
-    X(6, 2, 28, 10, 3)               \
-    X(7, 2, 28, 11, 3)              \
-    X(8, 2, 28, 11, 3)              \
-    X(1, 1, 30, 5, 4)               \
-    X(2, 1, 30, 6, 4)               \
-    X(3, 1, 30, 7, 4)               \
-    X(4, 1, 30, 8, 4)               \
-    X(5, 1, 30, 9, 4)               \
-    X(6, 1, 30, 10, 3)              \
-    X(7, 1, 22, 11, 3)              \
-    X(8, 1, 22, 11, 3)
+// (H, R1, T1, SU, SA, UNR): rows per thread, tile rows, u-ring stages, aux-ring stages,
+// queue unroll (ignored for H <= 3, which rotates the queue by renaming).
+#define SWB_TMA_VARIANTS(X)      \
+    X(1, 1, 30, 5, 4, 1)         \
+    X(2, 1, 30, 6, 4, 1)         \
+    X(3, 1, 30, 7, 4, 1)         \
+    X(4, 1, 30, 8, 4, 1)         \
+    X(4, 1, 30, 8, 4, 2)         \
+    X(4, 1, 30, 8, 4, 4)         \
+    X(5, 1, 30, 9, 4, 1)         \
+    X(5, 1, 30, 9, 4, 2)         \
+    X(6, 1, 30, 10, 3, 1)        \
+    X(6, 1, 30, 10, 3, 2)        \
+    X(6, 1, 30, 10, 3, 4)        \
+    X(7, 1, 22, 11, 3, 1)        \
+    X(7, 1, 22, 11, 3, 2)        \
+    X(8, 1, 22, 11, 3, 1)        \
+    X(8, 1, 22, 11, 3, 2)        \
+    X(8, 1, 22, 11, 3, 4)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
 
 struct Variant {
-    int H, R1, T1, SU, SA;
+    int H, R1, T1, SU, SA, UNR;
     KernelFn fn;
     size_t smem;
     int threads;
 };
 
-#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa) \
-    {h, r1, t1, su, sa, k_tma<h, r1, t1, su, sa>, smem_bytes<h, r1, t1, su, sa>(), Cfg<h, r1, t1>::NTHREADS},
+#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa, unr) \
+    {h, r1, t1, su, sa, unr, k_tma<h, r1, t1, su, sa, unr>, smem_bytes<h, r1, t1, su, sa>(), Cfg<h, r1, t1>::NTHREADS},
 
 // Rows per consumer thread: R1 = 1 doubles the consumer warps per SM (more latency hiding)
 // at the cost of re-reading the y-neighbour rows per row; SWB_R1=1|2 overrides the default.
@@ -429,9 +463,18 @@ int preferred_r1(int H) {
     return 1;
 }
 
+int preferred_unr(int H) {
+    const char* env = std::getenv("SWB_UNR");
+    if (env && env[0] >= '1' && env[0] <= '9') return env[0] - '0';
+    // measured on B200 at 256^3 and 512^3: 4 for SO 8 and 16, 2 for SO 10-14
+    return H == 4 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
+}
+
 const Variant* find_variant(int H) {
     static const Variant table[] = {SWB_TMA_VARIANTS(SWB_VARIANT_ENTRY)};
-    const int r1 = preferred_r1(H);
+    const int r1 = preferred_r1(H), unr = preferred_unr(H);
+    for (const auto& v : table)
+        if (v.H == H && v.R1 == r1 && v.UNR == unr) return &v;
     for (const auto& v : table)
         if (v.H == H && v.R1 == r1) return &v;
     for (const auto& v : table)
@@ -496,7 +539,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         smem = static_cast<int>(v->smem);
         fn = reinterpret_cast<const void*>(v->fn);
         p.kind = 0;
-        p.variant = 1000 + 100 * (v->R1 - 1) + H;
+        p.variant = 1000 + 100 * (v->R1 - 1) + 10 * v->UNR + H;
     }
     p.T1 = T1;
     p.T2 = kT2;
