@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(SqCfg<H, R1, T1, SU>::NTHREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: everything above overlapped the previous step's tail;
+    // u[t], u[t-1] written by that step are only touched after this point.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lt = c.step % 3, ln = (c.step + 1) % 3, lp = (c.step + 2) % 3;
     const int G = gridDim.x;
     const int nitems = sc.ncol * sc.nchunk;
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(SqCfg<H, R1, T1, SU>::NTHREADS, 1)
         }
     }
     __syncwarp();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     block_max_commit(mine, c.smax + c.slot);
 }
 
@@ -361,9 +365,8 @@ cudaError_t launch_sq(const TmaPlan& plan, const void* maps, const Geo& g, const
                       const Peer& p, const void* sched, cudaStream_t s) {
     const SqVariant* v = find_sq(plan.H);
     if (!v) return cudaErrorInvalidValue;
-    v->fn<<<plan.grid, v->threads, v->smem, s>>>(*static_cast<const Maps*>(maps), g, K, c, p,
-                                                 *static_cast<const Sched*>(sched));
-    return cudaGetLastError();
+    return launch_pdl(reinterpret_cast<const void*>(v->fn), plan.grid, v->threads, v->smem, s,
+                      *static_cast<const Maps*>(maps), g, K, c, p, *static_cast<const Sched*>(sched));
 }
 
 }  // namespace swb

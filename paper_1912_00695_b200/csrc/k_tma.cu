@@ -287,6 +287,9 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: everything above overlapped the previous step's tail;
+    // u[t], u[t-1] written by that step are only touched after this point.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     const int lt = c.step % 3, ln = (c.step + 1) % 3, lp = (c.step + 2) % 3;
     const int G = gridDim.x;
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         }
     }
     __syncwarp();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
     block_max_commit(mine, c.smax + c.slot);
     if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
@@ -642,8 +646,8 @@ cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, cons
     sc.zs = plan.zs;
     sc.x0 = g.x0;
     if (plan.kind == 1) return launch_sq(plan, maps, g, K, c, p, &sc, s);
-    v->fn<<<plan.grid, v->threads, v->smem, s>>>(*static_cast<const Maps*>(maps), g, K, c, p, sc);
-    return cudaGetLastError();
+    return launch_pdl(reinterpret_cast<const void*>(v->fn), plan.grid, v->threads, v->smem, s,
+                      *static_cast<const Maps*>(maps), g, K, c, p, sc);
 }
 
 }  // namespace swb

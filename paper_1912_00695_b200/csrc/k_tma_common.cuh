@@ -170,5 +170,25 @@ __device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned 
 // One arrival step of a consumer thread: take plane q's centre values into queue slot U,
 // and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
 // (U - H) mod NQ.  All queue indices are compile-time.
+// Launch a stencil kernel with programmatic stream serialization (PDL): the next step's
+// CTAs start their prologue while this step drains; they block in griddepcontrol.wait.
+inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
+                              const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
+                              const Sched& sc) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {const_cast<Maps*>(&maps), const_cast<Geo*>(&g), const_cast<Coef*>(&K),
+                    const_cast<Ctl*>(&c), const_cast<Peer*>(&p), const_cast<Sched*>(&sc)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 }  // namespace tma
 }  // namespace swb
