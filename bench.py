@@ -171,7 +171,9 @@ def run_ours(args, rank, world, local):
     prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
                                                    steps=nt_total))
     slab = D.slab_bounds(shape[0], world, rank) if world > 1 else None
-    m, damp = prob.m_data(), prob.damp_data()
+    m, damp = pinned(shape), pinned(shape)  # user-side host buffers in pinned memory
+    m[...] = prob.m_data()
+    damp[...] = prob.damp_data()
     op = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
     if world > 1:
         D.exchange_and_link(op, rank, world)

@@ -432,19 +432,14 @@ size_t smem_bytes() {
     X(1, 1, 30, 5, 4, 1)         \
     X(2, 1, 30, 6, 4, 1)         \
     X(3, 1, 30, 7, 4, 1)         \
-    X(4, 1, 30, 8, 4, 1)         \
-    X(4, 1, 30, 8, 4, 2)         \
     X(4, 1, 30, 8, 4, 4)         \
-    X(5, 1, 30, 9, 4, 1)         \
-    X(5, 1, 30, 9, 4, 2)         \
-    X(6, 1, 30, 10, 3, 1)        \
+    X(4, 1, 30, 11, 4, 4)        \
+    X(5, 1, 30, 10, 4, 2)        \
     X(6, 1, 30, 10, 3, 2)        \
-    X(6, 1, 30, 10, 3, 4)        \
-    X(7, 1, 22, 11, 3, 1)        \
-    X(7, 1, 22, 11, 3, 2)        \
-    X(8, 1, 22, 11, 3, 1)        \
-    X(8, 1, 22, 11, 3, 2)        \
-    X(8, 1, 22, 11, 3, 4)
+    X(6, 1, 30, 11, 3, 2)        \
+    X(7, 1, 22, 14, 3, 2)        \
+    X(8, 1, 22, 11, 3, 4)        \
+    X(8, 1, 22, 14, 3, 4)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
 
@@ -474,9 +469,18 @@ int preferred_unr(int H) {
     return H == 4 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
 }
 
+int preferred_su(int H) {
+    const char* env = std::getenv("SWB_SU");
+    if (env && env[0] >= '1' && env[0] <= '9') return std::atoi(env);
+    (void)H;
+    return 0;  // 0: first matching variant
+}
+
 const Variant* find_variant(int H) {
     static const Variant table[] = {SWB_TMA_VARIANTS(SWB_VARIANT_ENTRY)};
-    const int r1 = preferred_r1(H), unr = preferred_unr(H);
+    const int r1 = preferred_r1(H), unr = preferred_unr(H), su = preferred_su(H);
+    for (const auto& v : table)
+        if (v.H == H && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su)) return &v;
     for (const auto& v : table)
         if (v.H == H && v.R1 == r1 && v.UNR == unr) return &v;
     for (const auto& v : table)
@@ -603,6 +607,33 @@ cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* out)
 }
 
 static_assert(sizeof(Maps) == kTmaMapsBytes, "tensor-map block size");
+
+namespace {
+// flags[col * np + (x - x0)] = any damp != 0 over the output points of that tile and plane
+__global__ void k_damp_flags(const float* __restrict__ damp, long long plane, int P2, int x0, int np,
+                             int y0, int y1, int z0, int z1, int zs, int T1, int tiles_z,
+                             unsigned char* flags) {
+    const int col = blockIdx.y, x = x0 + blockIdx.x;
+    const int yt = y0 + (col / tiles_z) * T1, zt = zs + (col % tiles_z) * kT2;
+    const int ya = yt, yb = min(yt + T1, y1), za = max(zt, z0), zb = min(zt + kT2, z1);
+    int any = 0;
+    for (int t = threadIdx.x; t < (yb - ya) * kT2; t += blockDim.x) {
+        const int y = ya + t / kT2, z = zt + t % kT2;
+        if (z >= za && z < zb && damp[x * plane + static_cast<long long>(y) * P2 + z] != 0.0f) any = 1;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) flags[static_cast<long long>(col) * np + blockIdx.x] = static_cast<unsigned char>(any);
+}
+}  // namespace
+
+cudaError_t tma_damp_flags_device(const TmaPlan& plan, const Geo& g, unsigned char* flags, cudaStream_t s) {
+    const int np = g.x1 - g.x0;
+    if (np <= 0 || plan.columns <= 0) return cudaSuccess;
+    dim3 grid(np, plan.columns);
+    k_damp_flags<<<grid, 256, 0, s>>>(g.damp, g.plane, g.P2, g.x0, np, g.y0, g.y1, g.z0, g.z1, plan.zs,
+                                     plan.T1, plan.tiles_z, flags);
+    return cudaGetLastError();
+}
 
 void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp, int n1, int n2,
                     unsigned char* flags) {

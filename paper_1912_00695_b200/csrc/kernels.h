@@ -31,6 +31,8 @@ struct TmaPlan {
 // Host-side damp tile flags for a plan: flags[col * np + (x - x0)] = any damp != 0 in the tile.
 void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_local, int n1, int n2,
                     unsigned char* flags);
+// Same flags computed on the device from the uploaded damp field.
+cudaError_t tma_damp_flags_device(const TmaPlan& plan, const Geo& g, unsigned char* flags, cudaStream_t s);
 TmaPlan tma_plan(int H, const Geo& g, int num_sms);
 // Encodes the tensor maps for the three u levels (once per handle).
 constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps

@@ -416,10 +416,9 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         if (h->plan.ok && h->K.iso) {
             SWB_CUDA_C(tma_make_maps(h->plan, g, h->nl0, h->maps));
             const size_t nflags = static_cast<size_t>(h->plan.columns) * std::max(0, g.x1 - g.x0);
-            std::vector<unsigned char> flags(nflags);
-            tma_damp_flags(h->plan, g, p->damp, h->n1, h->n2, flags.data());
             SWB_CUDA_C(cudaMalloc(&h->d_dflag, std::max<size_t>(nflags, 1)));
-            SWB_CUDA_C(cudaMemcpy(h->d_dflag, flags.data(), nflags, cudaMemcpyHostToDevice));
+            SWB_CUDA_C(cudaMemsetAsync(h->d_dflag, 0, std::max<size_t>(nflags, 1), h->stream));
+            if (p->damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
             h->plan.dflag = h->d_dflag;
             h->use_tma = true;
         }
