@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "swb_internal.h"
+#include <climits>
 
 namespace swb {
 

@@ -313,6 +313,8 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             uint64_t pol_first;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
             unsigned st = 0, ph = 0;
+            bool lo_ready = c.ghost_lo_end <= 0 || c.need_lo == 0, hi_ready = !c.flags || c.need_hi == 0;
+            if (!c.flags) lo_ready = hi_ready = true;
             for (int item = blockIdx.x; item < nitems; item += G) {
                 const int col = item % sc.ncol, chunk = item / sc.ncol;
                 const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
@@ -325,6 +327,14 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                     const int nq = xb - xa + 2 * H;
                     for (int j = 0; j < nq; ++j) {
                         const int q = q0 + dir * j;
+                        if (q < c.ghost_lo_end && !lo_ready) {  // lower neighbour's step must be done
+                            wait_counter(c.flags, c.need_lo, c.err);
+                            lo_ready = true;
+                        }
+                        if (q >= c.ghost_hi_begin && !hi_ready) {
+                            wait_counter(c.flags + 1, c.need_hi, c.err);
+                            hi_ready = true;
+                        }
                         mbar_wait(empty_u + 8 * st, ph ^ 1u);
                         mbar_expect_tx(full_u + 8 * st, C::ROWS * C::W2 * 4);
                         tma_load3(uring_s + st * C::UPLANE, mu, zt - C::A, yt - H, q, full_u + 8 * st);
@@ -412,9 +422,11 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         }
     }
     __syncwarp();
+    if (c.sig_lo || c.sig_hi) __threadfence_system();  // peer stores of this thread -> system scope
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
     block_max_commit(mine, c.smax + c.slot);
+    signal_neighbours(c);
     if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
 }
 

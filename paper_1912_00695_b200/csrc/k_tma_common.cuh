@@ -170,6 +170,36 @@ __device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned 
 // One arrival step of a consumer thread: take plane q's centre values into queue slot U,
 // and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
 // (U - H) mod NQ.  All queue indices are compile-time.
+// Spin (acquire, system scope) until *flag >= need; bounded at ~20 s, then record an error
+// instead of hanging.  Followed by a proxy fence: the caller's next reads are TMA (async proxy).
+__device__ __forceinline__ void wait_counter(const unsigned long long* flag, unsigned long long need,
+                                             unsigned* err) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v < need) {
+        const unsigned long long t0 = gtimer();
+        while (true) {
+            __nanosleep(200);
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+            if (v >= need) break;
+            if (gtimer() - t0 > 20000000000ull) {
+                atomicExch(err, 1u);
+                break;
+            }
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// End-of-CTA signal for the fused halo exchange (after the CTA barrier in block_max_commit).
+__device__ __forceinline__ void signal_neighbours(const Ctl& c) {
+    if (threadIdx.x == 0 && (c.sig_lo || c.sig_hi)) {
+        __threadfence_system();
+        if (c.sig_lo) atomicAdd(c.sig_lo, 1ull);
+        if (c.sig_hi) atomicAdd(c.sig_hi, 1ull);
+    }
+}
+
 // Launch a stencil kernel with programmatic stream serialization (PDL): the next step's
 // CTAs start their prologue while this step drains; they block in griddepcontrol.wait.
 inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -37,6 +38,7 @@ constexpr uint32_t kBlobMagic = 0x53574231u;  // "SWB1"
 struct IpcBlob {
     uint32_t magic;
     int32_t xg_off, nl0, n1, n2, P2, H;
+    int32_t fused_capable, grid;
     int64_t level_floats;
     cudaIpcMemHandle_t u_handle;
     cudaIpcMemHandle_t flag_handle;
@@ -82,6 +84,9 @@ struct swb_handle {
     unsigned* d_err = nullptr;                // halo-exchange timeout flag
     unsigned long long* lo_remote = nullptr; // lower neighbour's d_flags[1]
     unsigned long long* hi_remote = nullptr; // upper neighbour's d_flags[0]
+    // per side: 1 = fused in-kernel ordering (both ends run the TMA kernel), 0 = wait/signal kernels
+    int fused_lo = 0, fused_hi = 0;
+    int nb_grid_lo = 0, nb_grid_hi = 0;      // neighbours' CTAs per step (fused counters)
     void* ipc_lo_u = nullptr;
     void* ipc_hi_u = nullptr;
     void* ipc_lo_f = nullptr;
@@ -175,17 +180,32 @@ int refresh_ring(swb_handle* h) {
 }
 
 int enqueue_steps(swb_handle* h, int step0, int nt) {
+    const int kmask = (h->lo_remote && !h->fused_lo ? 1 : 0) | (h->hi_remote && !h->fused_hi ? 2 : 0);
     for (int i = 0; i < nt; ++i) {
         const int s = step0 + i;
-        const bool linked = h->lo_remote || h->hi_remote;
-        if (linked) {
-            const int mask = (h->lo_remote ? 1 : 0) | (h->hi_remote ? 2 : 0);
-            SWB_CUDA(launch_wait_flags(h->d_flags, mask, h->steps_done + i, h->d_err, h->stream));
+        if (kmask) {  // kernel-based ordering for sides without fused support
+            SWB_CUDA(launch_wait_flags(h->d_flags, kmask, h->steps_done + i, h->d_err, h->stream));
             ++h->launches;
         }
         Ctl c = h->ctl;
         c.step = s;
         c.slot = i;
+        c.err = h->d_err;
+        c.ghost_lo_end = 0;
+        c.ghost_hi_begin = INT_MAX;
+        if ((h->lo_remote && h->fused_lo) || (h->hi_remote && h->fused_hi)) {
+            c.flags = h->d_flags;
+            if (h->lo_remote && h->fused_lo) {
+                c.sig_lo = h->lo_remote;
+                c.need_lo = static_cast<unsigned long long>(h->nb_grid_lo) * (h->steps_done + i);
+                c.ghost_lo_end = h->gb;
+            }
+            if (h->hi_remote && h->fused_hi) {
+                c.sig_hi = h->hi_remote;
+                c.need_hi = static_cast<unsigned long long>(h->nb_grid_hi) * (h->steps_done + i);
+                c.ghost_hi_begin = h->gb + (h->hi - h->lo);
+            }
+        }
         if (h->use_tma) {
             SWB_CUDA(launch_tma(h->plan, h->maps, h->geo, h->K, c, h->peer, h->stream));
         } else {
@@ -202,15 +222,17 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
                                       h->d_traces + static_cast<long long>(i) * owned, h->stream));
             ++h->launches;
         }
-        if (linked) {
-            SWB_CUDA(launch_signal_flags(h->lo_remote, h->hi_remote, h->steps_done + i + 1,
-                                         h->stream));
+        if (kmask) {
+            SWB_CUDA(launch_signal_flags(kmask & 1 ? h->lo_remote : nullptr, kmask & 2 ? h->hi_remote : nullptr,
+                                         h->steps_done + i + 1, h->stream));
             ++h->launches;
         }
     }
     h->steps_done += nt;
     return SWB_OK;
 }
+
+bool fused_capable(const swb_handle* h) { return h->use_tma && h->plan.kind == 0; }
 
 void compute_peer_ranges(swb_handle* h) {
     // planes mirrored to the lower neighbour: global [lo, lo+HU) ∩ updated; upper: [hi-HU, hi) ∩ updated
@@ -412,6 +434,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     if (h->form == SWB_FORM_FACTORISED) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+        if (const char* cap = std::getenv("SWB_MAX_CTAS")) sms = std::max(1, std::min(sms, std::atoi(cap)));
         h->plan = tma_plan(HU, g, sms);
         if (h->plan.ok && h->K.iso) {
             SWB_CUDA_C(tma_make_maps(h->plan, g, h->nl0, h->maps));
@@ -624,6 +647,15 @@ int swb_link_local(swb_handle* lower, swb_handle* upper) {
     upper->peer.lo_shift = upper->xg_off - lower->xg_off;
     lower->hi_remote = upper->d_flags + 0;
     upper->lo_remote = lower->d_flags + 1;
+    // Same-device slabs run their persistent kernels concurrently on one GPU: in-kernel waits
+    // are only safe if both grids fit at once, so they are opt-in there (tests cap the grid
+    // with SWB_MAX_CTAS).  Across devices they are always safe.
+    const bool same_dev = lower->device == upper->device;
+    const int fused = fused_capable(lower) && fused_capable(upper) &&
+                      (!same_dev || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
+    lower->fused_hi = upper->fused_lo = fused;
+    lower->nb_grid_hi = upper->plan.grid;
+    upper->nb_grid_lo = lower->plan.grid;
     compute_peer_ranges(lower);
     compute_peer_ranges(upper);
     return SWB_OK;
@@ -644,6 +676,8 @@ int swb_export_ghosts(swb_handle* h, void* blob, size_t* blob_len) {
     b.n2 = h->n2;
     b.P2 = h->P2;
     b.H = h->HU;
+    b.fused_capable = fused_capable(h) ? 1 : 0;
+    b.grid = h->plan.grid;
     b.level_floats = h->level_floats;
     SWB_CUDA(cudaIpcGetMemHandle(&b.u_handle, h->u));
     SWB_CUDA(cudaIpcGetMemHandle(&b.flag_handle, h->d_flags));
@@ -673,6 +707,8 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         for (int l = 0; l < 3; ++l) h->peer.lo_lev[l] = base + l * b.level_floats;
         h->peer.lo_shift = h->xg_off - b.xg_off;
         h->lo_remote = static_cast<unsigned long long*>(h->ipc_lo_f) + 1;
+        h->fused_lo = b.fused_capable && fused_capable(h);
+        h->nb_grid_lo = b.grid;
     }
     if (upper_blob && upper_len) {
         IpcBlob b;
@@ -682,6 +718,8 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         for (int l = 0; l < 3; ++l) h->peer.hi_lev[l] = base + l * b.level_floats;
         h->peer.hi_shift = h->xg_off - b.xg_off;
         h->hi_remote = static_cast<unsigned long long*>(h->ipc_hi_f) + 0;
+        h->fused_hi = b.fused_capable && fused_capable(h);
+        h->nb_grid_hi = b.grid;
     }
     compute_peer_ranges(h);
     return SWB_OK;

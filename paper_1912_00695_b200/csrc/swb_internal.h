@@ -55,6 +55,17 @@ struct Ctl {
     int step;               // absolute step
     int slot;               // index into smax / traces for this step
     unsigned long long* trace;  // optional per-CTA timestamps [gridDim][4] (SWB_TRACE), or null
+    // Fused halo-exchange ordering (TMA kernel on linked z-slabs; all null/0 otherwise):
+    // every CTA bumps sig_lo / sig_hi (counters in the neighbours' memory) once it has
+    // finished the step, and a producer about to TMA-load a ghost plane first waits until
+    // flags[0] (lower neighbour) / flags[1] (upper) reach need_lo / need_hi.
+    unsigned long long* sig_lo;
+    unsigned long long* sig_hi;
+    const unsigned long long* flags;
+    unsigned long long need_lo, need_hi;
+    int ghost_lo_end;           // local planes < ghost_lo_end are lower ghosts (0: none)
+    int ghost_hi_begin;         // local planes >= ghost_hi_begin are upper ghosts (INT_MAX: none)
+    unsigned* err;              // set to 1 if a wait timed out
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -172,3 +172,34 @@ def test_local_slabs_bitwise_equal_single_domain(form, cuts):
             lo_, hi_ = o.slab
             full[lo_:hi_] = part[lo_:hi_]
         assert np.array_equal(full, whole.get_level(l)), l
+
+
+@pytest.mark.parametrize("cuts", [(14,), (9, 19)])
+def test_local_slabs_fused_exchange_bitwise(cuts, monkeypatch):
+    """Fused in-kernel halo ordering (producers wait on the neighbours' step counters, every
+    CTA signals at exit) on one GPU: grids are capped so all slabs' persistent kernels are
+    co-resident, as they are on separate GPUs."""
+    monkeypatch.setenv("SWB_FUSED_SAME_DEVICE", "1")
+    monkeypatch.setenv("SWB_MAX_CTAS", str(148 // (len(cuts) + 1)))
+    shape, so, nt = (40, 64, 70), 8, 13
+    rng = np.random.default_rng(9)
+    vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
+                              velocity_field=vel, damp_max=0.05, damp_width=4, source_point=[20, 32, 35])
+    prob = P.make_wave_problem(cfg)
+    whole = P.Operator(prob)
+    wr = whole.apply(nt, 0)
+    bounds = [0] + list(cuts) + [shape[0]]
+    ops = [P.Operator(prob, slab=(bounds[i], bounds[i + 1])) for i in range(len(bounds) - 1)]
+    for lo, hi in zip(ops[:-1], ops[1:]):
+        P.Operator.link_local(lo, hi)
+    for o in ops:
+        o.apply_async(nt, 0)
+    smax = np.max([o.collect(nt) for o in ops], axis=0)
+    assert np.array_equal(smax, wr.step_max_abs)
+    for l in range(3):
+        full = np.zeros(shape, np.float32)
+        for o in ops:
+            lo_, hi_ = o.slab
+            full[lo_:hi_] = o.get_level(l)[lo_:hi_]
+        assert np.array_equal(full, whole.get_level(l)), l
