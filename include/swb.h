@@ -86,6 +86,12 @@ typedef struct swb_problem {
      * of the global grid; slab_hi <= 0 means the whole grid.  See swb_link_neighbours. */
     int32_t slab_lo;
     int32_t slab_hi;
+    /* Off-grid receivers (new; Devito-style trilinear interpolation): physical coordinates
+     * [n_coord_receivers][3] with grid index 0 at coordinate 0.  Their traces follow the
+     * on-grid receivers' in rec_traces.  Value = sum over the 8 surrounding cells, in
+     * (a,b,c) lexicographic order, of ((wx_a*wy_b)*wz_c)*u in double, w0 = 1-f, w1 = f. */
+    int32_t n_coord_receivers;
+    const double* coord_receivers;
 } swb_problem;
 
 typedef struct swb_handle swb_handle;

@@ -140,7 +140,7 @@ def _fptr(a: Optional[np.ndarray]):
 
 
 def _run(which: str, cfg: OracleConfig, *, dse: str = "basic", threads: int = 0,
-         serial: bool = False, initial_u=None, receivers=None) -> dict:
+         serial: bool = False, initial_u=None, receivers=None, receiver_coords=None) -> dict:
     lib = _lib(which)
     c = cfg.to_c()
     n = cfg.ncells
@@ -166,12 +166,21 @@ def _run(which: str, cfg: OracleConfig, *, dse: str = "basic", threads: int = 0,
                          1 if serial else 0, init_arr, n_init, n_rec, rec_ptr, C.byref(out))
         err = lib.ref_last_error
     else:
-        rc = lib.port_run(C.byref(c), int(threads), init_arr, n_init, n_rec, rec_ptr, C.byref(out))
+        crec = None if receiver_coords is None else np.ascontiguousarray(receiver_coords, np.float64).reshape(-1, 3)
+        n_crec = 0 if crec is None else crec.shape[0]
+        ctr = np.zeros((cfg.steps, max(n_crec, 1)), np.float32)
+        rc = lib.port_run2(C.byref(c), int(threads), init_arr, n_init, n_rec, rec_ptr, n_crec,
+                           crec.ctypes.data_as(C.POINTER(C.c_double)) if n_crec else C.POINTER(C.c_double)(),
+                           _fptr(ctr) if n_crec else C.POINTER(C.c_float)(), C.byref(out))
         err = lib.port_last_error
     if rc != 0:
         raise OracleError(rc, err().decode(), out.bad_step)
     shape = tuple(cfg.shape)
+    coord_traces = None
+    if which == "port" and receiver_coords is not None:
+        coord_traces = ctr[:, :n_crec]
     return {
+        "coord_traces": coord_traces,
         "levels": levels.reshape((3,) + shape),
         "step_max_abs": smax,
         "rec_traces": traces[:, :n_rec] if n_rec else None,
@@ -183,6 +192,9 @@ def _run(which: str, cfg: OracleConfig, *, dse: str = "basic", threads: int = 0,
 
 def ref_run(cfg: OracleConfig, **kw) -> dict:
     """exec::run (or exec::reference_run with serial=True) of the reference itself."""
+    if kw.get("receiver_coords") is not None:
+        raise ValueError("the reference has no off-grid receivers (use port_run)")
+    kw.pop("receiver_coords", None)
     return _run("ref", cfg, **kw)
 
 

@@ -259,9 +259,46 @@ static inline float point_update(const port_problem* p, const float* ut, const f
     return (float)acc;
 }
 
+/* Trilinear receiver sampling restated for the off-grid receivers (an addition: the reference
+ * samples only through on_step at grid points).  Index position g = X/h (h = float spacing
+ * widened), i0 = floor(g) clamped to n-2, f = g - i0, weights w0 = 1-f, w1 = f; the value is
+ * sum over corners (a,b,c) in lexicographic order of ((wx*wy)*wz)*u, in double, no FMA. */
+static int crec_stencil(const port_problem* p, const double* X, size_t* idx, double* w) {
+    const int n[3] = {p->n0, p->n1, p->n2};
+    int i0[3];
+    double f[3];
+    for (int d = 0; d < 3; ++d) {
+        double g = X[d] / (double)p->h[d];
+        if (!(g >= 0.0) || g > (double)(n[d] - 1)) return 1;
+        int i = (int)floor(g);
+        if (i >= n[d] - 1) i = n[d] - 2;
+        i0[d] = i;
+        f[d] = g - (double)i;
+    }
+    int c = 0;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int e = 0; e < 2; ++e, ++c) {
+                double wa = a ? f[0] : 1.0 - f[0], wb = b ? f[1] : 1.0 - f[1], we = e ? f[2] : 1.0 - f[2];
+                w[c] = (wa * wb) * we;
+                idx[c] = ((size_t)(i0[0] + a) * n[1] + (size_t)(i0[1] + b)) * n[2] + (size_t)(i0[2] + e);
+            }
+    return 0;
+}
+
+int port_run2(const port_config* c, int threads, const float* const* initial_u, int n_initial,
+              int n_rec, const int32_t* rec, int n_crec, const double* crec, float* crec_traces,
+              port_run_out* out);
+
 /* exec::run on the basic IET, restated.  levels: caller-owned [3][n]; initial_u optional. */
 int port_run(const port_config* c, int threads, const float* const* initial_u, int n_initial,
              int n_rec, const int32_t* rec, port_run_out* out) {
+    return port_run2(c, threads, initial_u, n_initial, n_rec, rec, 0, NULL, NULL, out);
+}
+
+int port_run2(const port_config* c, int threads, const float* const* initial_u, int n_initial,
+              int n_rec, const int32_t* rec, int n_crec, const double* crec, float* crec_traces,
+              port_run_out* out) {
     port_problem p;
     int rc = port_make(c, &p);
     if (rc) return rc;
@@ -270,6 +307,18 @@ int port_run(const port_config* c, int threads, const float* const* initial_u, i
     for (int d = 0; d < 3; ++d)
         if (c->shape[d] - 1 - H < H) {
             port_free(&p); strcpy(g_err, "grid extent is too small for halo"); return 1; }
+    size_t* cidx = NULL;
+    double* cw = NULL;
+    if (n_crec > 0) {
+        cidx = (size_t*)malloc(sizeof(size_t) * 8 * (size_t)n_crec);
+        cw = (double*)malloc(sizeof(double) * 8 * (size_t)n_crec);
+        for (int r = 0; r < n_crec; ++r)
+            if (crec_stencil(&p, crec + 3 * r, cidx + 8 * r, cw + 8 * r)) {
+                free(cidx); free(cw); port_free(&p);
+                snprintf(g_err, sizeof g_err, "receiver coordinate %d lies outside the grid", r);
+                return 1;
+            }
+    }
     float* u = (float*)calloc(3 * n, sizeof(float));
     if (initial_u)
         for (int l = 0; l < n_initial && l < 3; ++l) memcpy(u + n * l, initial_u[l], n * sizeof(float));
@@ -320,7 +369,7 @@ int port_run(const port_config* c, int threads, const float* const* initial_u, i
         }
         if (!finite) {
             out->bad_step = step;
-            free(u); port_free(&p);
+            free(u); free(cidx); free(cw); port_free(&p);
             snprintf(g_err, sizeof g_err, "non-finite wave field at step %d (unstable dt?)", step);
             return 3;
         }
@@ -329,6 +378,12 @@ int port_run(const port_config* c, int threads, const float* const* initial_u, i
             for (int r = 0; r < n_rec; ++r)
                 out->rec_traces[(size_t)step * n_rec + r] =
                     up1[(size_t)rec[3 * r] * s0 + (size_t)rec[3 * r + 1] * s1 + (size_t)rec[3 * r + 2]];
+        if (crec_traces)
+            for (int r = 0; r < n_crec; ++r) {
+                double v = 0.0;
+                for (int k = 0; k < 8; ++k) v = v + cw[8 * r + k] * (double)up1[cidx[8 * r + k]];
+                crec_traces[(size_t)step * n_crec + r] = (float)v;
+            }
     }
     double t1 = 0;
 #ifdef _OPENMP
@@ -339,6 +394,8 @@ int port_run(const port_config* c, int threads, const float* const* initial_u, i
     out->point_updates = updates;
     out->final_level = p.steps % 3;
     free(u);
+    free(cidx);
+    free(cw);
     port_free(&p);
     return 0;
 }

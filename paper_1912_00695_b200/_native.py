@@ -25,7 +25,8 @@ class SwbProblem(C.Structure):
         ("wavelet", C.POINTER(C.c_float)), ("wavelet_len", C.c_int32),
         ("n_receivers", C.c_int32), ("receivers", C.POINTER(C.c_int32)), ("form", C.c_int32),
         ("time_block", C.c_int32), ("device", C.c_int32), ("slab_lo", C.c_int32),
-        ("slab_hi", C.c_int32),
+        ("slab_hi", C.c_int32), ("n_coord_receivers", C.c_int32),
+        ("coord_receivers", C.POINTER(C.c_double)),
     ]
 
 

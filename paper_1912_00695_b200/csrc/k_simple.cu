@@ -120,6 +120,31 @@ __global__ void k_receivers(const float* __restrict__ un, const long long* __res
     }
 }
 
+// Receiver sampling through 8-corner stencils (on-grid receivers: one corner of weight 1, so the
+// trace is exactly u; off-grid: trilinear weights).  Double accumulation in a fixed order, no
+// FMA, so the result is bit-identical to the C oracle's restatement.  Corners not owned by this
+// slab have index -1 (their partial sums are added across slabs by the caller).
+__global__ void k_samplers(const float* __restrict__ un, const long long* __restrict__ idx,
+                           const double* __restrict__ w, int n, float* __restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) {
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const long long j = idx[8 * r + c];
+            if (j >= 0) v = __dadd_rn(v, __dmul_rn(w[8 * r + c], static_cast<double>(un[j])));
+        }
+        out[r] = static_cast<float>(v);
+    }
+}
+
+cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
+                            cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_samplers<<<ceil_div(n, 128), 128, 0, s>>>(un, idx, w, n, out);
+    return cudaGetLastError();
+}
+
 // Halo-exchange ordering: spin until every linked neighbour has completed at least
 // `need` steps (counters live in this handle's memory and are written by the neighbours).
 // Bounded: after `timeout_ns` the kernel records an error instead of hanging the device.

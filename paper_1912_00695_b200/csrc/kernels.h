@@ -45,6 +45,8 @@ cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, in
                             int z_in1, unsigned* out, cudaStream_t s);
 cudaError_t launch_receivers(const float* un, const long long* idx, int n, float* out,
                              cudaStream_t s);
+cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
+                            cudaStream_t s);
 cudaError_t launch_wait_flags(const unsigned long long* flags, int mask,
                               unsigned long long need, unsigned* err, cudaStream_t s);
 cudaError_t launch_signal_flags(unsigned long long* lo_flag, unsigned long long* hi_flag,

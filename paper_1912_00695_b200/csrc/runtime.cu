@@ -66,7 +66,8 @@ struct swb_handle {
     // receivers
     int n_rec = 0;
     std::vector<int> rec_owned;          // global receiver index per owned receiver
-    long long* d_rec_idx = nullptr;      // local flat index per owned receiver
+    long long* d_rec_idx = nullptr;      // [owned][8] local flat corner indices (-1: not owned)
+    double* d_rec_w = nullptr;           // [owned][8] corner weights
     float* d_traces = nullptr;
     int traces_cap = 0;
     // stencil
@@ -218,8 +219,8 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
         ++h->launches;
         if (!h->rec_owned.empty()) {
             const int owned = static_cast<int>(h->rec_owned.size());
-            SWB_CUDA(launch_receivers(h->u + ((s + 1) % 3) * h->level_floats, h->d_rec_idx, owned,
-                                      h->d_traces + static_cast<long long>(i) * owned, h->stream));
+            SWB_CUDA(launch_samplers(h->u + ((s + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w, owned,
+                                     h->d_traces + static_cast<long long>(i) * owned, h->stream));
             ++h->launches;
         }
         if (kmask) {
@@ -303,6 +304,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     }
     if (p->n_receivers < 0 || (p->n_receivers > 0 && !p->receivers))
         return fail(SWB_EINVAL, "bad receiver list");
+    if (p->n_coord_receivers < 0 || (p->n_coord_receivers > 0 && !p->coord_receivers))
+        return fail(SWB_EINVAL, "bad coordinate receiver list");
     for (int r = 0; r < p->n_receivers; ++r)
         for (int d = 0; d < 3; ++d)
             if (p->receivers[3 * r + d] < 0 || p->receivers[3 * r + d] >= p->shape[d])
@@ -416,19 +419,65 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     }
     c.wavelet = h->d_wavelet;
     c.wavelet_len = h->wavelet_len;
-    h->n_rec = p->n_receivers;
+    // Receivers: every sampling point becomes an 8-corner stencil over this slab's planes.
+    h->n_rec = p->n_receivers + std::max(0, p->n_coord_receivers);
     std::vector<long long> ridx;
+    std::vector<double> rw;
+    auto local_index = [&](int x, int y, int z) -> long long {
+        if (x < lo || x >= hi) return -1;
+        return (x - h->xg_off) * h->plane + static_cast<long long>(y) * h->P2 + z;
+    };
     for (int r = 0; r < p->n_receivers; ++r) {
         const int* q = p->receivers + 3 * r;
         if (q[0] >= lo && q[0] < hi) {
             h->rec_owned.push_back(r);
-            ridx.push_back((q[0] - h->xg_off) * h->plane + static_cast<long long>(q[1]) * h->P2 + q[2]);
+            ridx.push_back(local_index(q[0], q[1], q[2]));
+            rw.push_back(1.0);
+            for (int c = 1; c < 8; ++c) {
+                ridx.push_back(-1);
+                rw.push_back(0.0);
+            }
+        }
+    }
+    for (int r = 0; r < std::max(0, p->n_coord_receivers); ++r) {
+        const double* X = p->coord_receivers + 3 * r;
+        int i0[3];
+        double f[3];
+        for (int d = 0; d < 3; ++d) {
+            const double hd = static_cast<double>(p->spacing[d]);
+            const double gx = X[d] / hd;
+            if (!(gx >= 0.0) || gx > static_cast<double>(p->shape[d] - 1))
+                return cleanup(fail(SWB_EINVAL, "receiver coordinate " + std::to_string(r) + " lies outside the grid"));
+            int i = static_cast<int>(std::floor(gx));
+            if (i >= p->shape[d] - 1) i = p->shape[d] - 2;
+            i0[d] = i;
+            f[d] = gx - static_cast<double>(i);
+        }
+        std::vector<long long> ci(8);
+        std::vector<double> cw(8);
+        bool any = false;
+        int c = 0;
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+                for (int e = 0; e < 2; ++e, ++c) {
+                    const double wa = a ? f[0] : 1.0 - f[0], wb = b ? f[1] : 1.0 - f[1], we = e ? f[2] : 1.0 - f[2];
+                    cw[c] = (wa * wb) * we;
+                    ci[c] = local_index(i0[0] + a, i0[1] + b, i0[2] + e);
+                    any |= ci[c] >= 0;
+                }
+        if (any) {
+            h->rec_owned.push_back(p->n_receivers + r);
+            ridx.insert(ridx.end(), ci.begin(), ci.end());
+            rw.insert(rw.end(), cw.begin(), cw.end());
         }
     }
     if (!ridx.empty()) {
         SWB_CUDA_C(cudaMalloc(&h->d_rec_idx, sizeof(long long) * ridx.size()));
+        SWB_CUDA_C(cudaMalloc(&h->d_rec_w, sizeof(double) * rw.size()));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_idx, ridx.data(), sizeof(long long) * ridx.size(),
                                    cudaMemcpyHostToDevice, h->stream));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_w, rw.data(), sizeof(double) * rw.size(), cudaMemcpyHostToDevice,
+                                   h->stream));
     }
     // Kernel choice: the TMA 2.5D kernel for the factorised form when the plan fits.
     if (h->form == SWB_FORM_FACTORISED) {
@@ -606,6 +655,7 @@ int swb_destroy(swb_handle* h) {
     for (void* q : {static_cast<void*>(h->u), static_cast<void*>(h->m), static_cast<void*>(h->damp),
                     static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
                     static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
+                    static_cast<void*>(h->d_rec_w),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
                     static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err),
                     static_cast<void*>(h->d_trace)})

@@ -317,6 +317,7 @@ class Operator:
 
     def __init__(self, problem: WaveProblem, dse: DseLevel = DseLevel.aggressive, *,
                  form: Optional[str] = None, receivers: Optional[np.ndarray] = None,
+                 receiver_coords: Optional[np.ndarray] = None,
                  device: int = 0, time_block: int = 1,
                  slab: Optional[Tuple[int, int]] = None,
                  m: Optional[np.ndarray] = None, damp: Optional[np.ndarray] = None):
@@ -357,6 +358,13 @@ class Operator:
             self.receivers = rec
             p.n_receivers = rec.shape[0]
             p.receivers = rec.ctypes.data_as(C.POINTER(C.c_int32))
+        self.receiver_coords = None
+        if receiver_coords is not None:
+            rc = np.ascontiguousarray(receiver_coords, np.float64).reshape(-1, 3)
+            self._keep.append(rc)
+            self.receiver_coords = rc
+            p.n_coord_receivers = rc.shape[0]
+            p.coord_receivers = rc.ctypes.data_as(C.POINTER(C.c_double))
         p.form = _FORMS[self.form]
         p.time_block = int(time_block)
         p.device = int(device)
@@ -390,7 +398,8 @@ class Operator:
         step0 = self.step if step0 is None else int(step0)
         smax = np.zeros(nt, np.float32)
         bad = C.c_int32(-1)
-        n_rec = 0 if self.receivers is None else self.receivers.shape[0]
+        n_rec = (0 if self.receivers is None else self.receivers.shape[0]) + \
+            (0 if self.receiver_coords is None else self.receiver_coords.shape[0])
         traces = np.zeros((nt, n_rec), np.float32) if n_rec else None
         t0 = time.perf_counter()
         rc = N.lib.swb_apply(self._h, step0, nt, N.fptr(smax), C.byref(bad),
@@ -455,14 +464,16 @@ class Operator:
 
 def run(problem: WaveProblem, options: Optional[RunOptions] = None,
         dse: DseLevel = DseLevel.aggressive, *, form: Optional[str] = None,
-        receivers: Optional[np.ndarray] = None, device: int = 0) -> RunResult:
+        receivers: Optional[np.ndarray] = None, receiver_coords: Optional[np.ndarray] = None,
+        device: int = 0) -> RunResult:
     """exec::run (include/stencilc/executor.hpp:90-91, src/executor.cpp:546-613).
 
     The IET argument of the reference is identified by its DSE level: the acoustic IET
     built by lower -> optimize_all(dse) -> build_iet for this problem.
     """
     options = options or RunOptions()
-    op = Operator(problem, dse, form=form, receivers=receivers, device=device)
+    op = Operator(problem, dse, form=form, receivers=receivers, receiver_coords=receiver_coords,
+                  device=device)
     try:
         if options.initial_u is not None:
             if len(options.initial_u) > 3:

@@ -203,3 +203,27 @@ def test_local_slabs_fused_exchange_bitwise(cuts, monkeypatch):
             lo_, hi_ = o.slab
             full[lo_:hi_] = o.get_level(l)[lo_:hi_]
         assert np.array_equal(full, whole.get_level(l)), l
+
+
+@pytest.mark.parametrize("form", ["plain_f64", "factorised"])
+def test_offgrid_receivers_trilinear(form):
+    """Off-grid receivers: trilinear interpolation restated in the C oracle; bit-exact for the
+    bit-exact kernel (same double op order), <= 1e-5 for the factorised kernel."""
+    shape, so, nt = (28, 30, 32), 8, 15
+    rng = np.random.default_rng(4)
+    coords = np.stack([rng.uniform(0, (s - 1) * 10.0, 40) for s in shape], axis=1)
+    coords[0] = [140.0, 150.0, 160.0]        # exactly on a grid point
+    coords[1] = [270.0, 290.0, 310.0]        # the last grid point (clamped cell)
+    grid_rec = np.array([[14, 15, 16]], np.int32)
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt)
+    res = P.run(P.make_wave_problem(cfg), form=form, receivers=grid_rec, receiver_coords=coords)
+    ref = O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=nt), receivers=grid_rec,
+                     receiver_coords=coords)
+    got = res.rec_traces[:, 1:]
+    assert np.array_equal(res.rec_traces[:, 0], got[:, 0])  # on-grid coordinate == integer receiver
+    if form == "plain_f64":
+        assert np.array_equal(got, ref["coord_traces"])
+    else:
+        assert rel_l2(got, ref["coord_traces"]) <= TOL
+    with pytest.raises(ValueError, match="outside the grid"):
+        P.Operator(P.make_wave_problem(cfg), receiver_coords=[[-1.0, 5.0, 5.0]])
