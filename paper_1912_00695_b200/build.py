@@ -13,9 +13,10 @@ ROOT = os.path.dirname(HERE)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
     "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
 ]
+OBJ = os.path.join(HERE, "_lib", "obj")
 
 
 def sources():
@@ -44,12 +45,25 @@ def nvcc() -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(OBJ, exist_ok=True)
+    # one nvcc per translation unit, in parallel (the kernel TUs dominate), then one link
+    from concurrent.futures import ThreadPoolExecutor
+    objs = []
+    cmds = []
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmds.append([nvcc()] + NVCC_FLAGS + ["-c", "-o", obj, src])
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        for cmd in cmds:
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+        list(ex.map(lambda c: subprocess.run(c, check=True, cwd=ROOT), cmds))
     tmp = OUT + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", tmp] + sources()
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True, cwd=ROOT)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True, cwd=ROOT)
     os.replace(tmp, OUT)
     return OUT
 
