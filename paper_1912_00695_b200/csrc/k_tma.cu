@@ -38,6 +38,15 @@ namespace swb {
 namespace {
 using namespace tma;
 
+// K3 stage-1 progress publication: a plane counts as done once every consumer warp has
+// stored its rows of it (warps drift apart by up to SU-H planes, so a per-plane smem tally
+// over a ring of 16 slots finds the last warp, which publishes with atomicMax).
+struct Pub {
+    unsigned long long* cnt;  // this item's global counter (null: not publishing)
+    unsigned long long base;  // epoch tag
+    unsigned* done;           // smem [16] per-plane warp tallies
+};
+
 template <int H, int R1, int T1, int SU, int SA, int QN, int U>
 __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const Item& it,
                                               const float* ucol, const float* acol,
@@ -47,7 +56,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
                                               unsigned& sa, unsigned& pa_, unsigned& mine,
                                               float* un, float* lo_peer, float* hi_peer,
                                               const Geo& g, const Coef& K, const Ctl& c,
-                                              const Peer& pr) {
+                                              const Peer& pr, const Pub& pub) {
     using C = Cfg<H, R1, T1>;
     constexpr int NQ = QN;  // queue slots; plane j-m sits in slot (U - m) mod QN
     const int q = it.q0 + it.dir * j;
@@ -170,28 +179,42 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
         for (int i = 0; i < R1; ++i)
             if (it.rows_ok || it.yt + i < g.y1)
                 store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int i = 0; i < R1; ++i) {
-        const int y = it.yt + i;
-        float4 o = out[i];
-        if (y >= g.y1) continue;
-        if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
-            const int e = c.src_z - it.zc;
-            set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
-                                         static_cast<double>(K.dt)));
+        for (int i = 0; i < R1; ++i) {
+            const int y = it.yt + i;
+            float4 o = out[i];
+            if (y >= g.y1) continue;
+            if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
+                const int e = c.src_z - it.zc;
+                set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
+                                             static_cast<double>(K.dt)));
+            }
+            const long long idx = xoff + static_cast<long long>(i) * g.P2;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int z = it.zc + e;
+                if (z >= g.z0 && z < g.z1) {
+                    const float v = comp(o, e);
+                    un[idx + e] = v;
+                    if (lo_m) lo_peer[idx + e + static_cast<long long>(pr.lo_shift) * g.plane] = v;
+                    if (hi_m) hi_peer[idx + e + static_cast<long long>(pr.hi_shift) * g.plane] = v;
+                    mine = max(mine, abs_bits(v));
+                }
+            }
         }
-        const long long idx = xoff + static_cast<long long>(i) * g.P2;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int z = it.zc + e;
-            if (z >= g.z0 && z < g.z1) {
-                const float v = comp(o, e);
-                un[idx + e] = v;
-                if (lo_m) lo_peer[idx + e + static_cast<long long>(pr.lo_shift) * g.plane] = v;
-                if (hi_m) hi_peer[idx + e + static_cast<long long>(pr.hi_shift) * g.plane] = v;
-                mine = max(mine, abs_bits(v));
+    }
+    // Temporal blocking, stage 1: publish "this warp has stored one more u[t+1] plane"
+    // (the stage-2 CTAs wait on these counters before reading the plane through TMA).
+    if (pub.cnt) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            __threadfence();  // this warp's stores (seen through __syncwarp) before the tally
+            const int n = j - 2 * H;  // output plane index within the item
+            const unsigned old = atomicAdd(pub.done + (n & 15), 1u);
+            if (old == C::NCW - 1) {  // last warp for this plane: publish
+                pub.done[n & 15] = 0u;
+                atomicMax(pub.cnt, pub.base + static_cast<unsigned long long>(n + 1));
             }
         }
     }
@@ -206,14 +229,14 @@ struct Unrolled {
                                                unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
                                                unsigned& mine, float* un, float* lo_peer,
                                                float* hi_peer, const Geo& g, const Coef& K,
-                                               const Ctl& c, const Peer& pr) {
+                                               const Ctl& c, const Peer& pr, const Pub& pub) {
         if (jb + U < it.nq) {
             consumer_step<H, R1, T1, SU, SA, 2 * H + 1, U>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
                                                 full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                lo_peer, hi_peer, g, K, c, pr);
+                                                lo_peer, hi_peer, g, K, c, pr, pub);
             Unrolled<H, R1, T1, SU, SA, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                     full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                    lo_peer, hi_peer, g, K, c, pr);
+                                                    lo_peer, hi_peer, g, K, c, pr, pub);
         }
     }
 };
@@ -224,7 +247,7 @@ struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
                                                unsigned, unsigned, unsigned, unsigned&, unsigned&,
                                                unsigned&, unsigned&, unsigned&, unsigned&, float*,
                                                float*, float*, const Geo&, const Coef&, const Ctl&,
-                                               const Peer&) {}
+                                               const Peer&, const Pub&) {}
 };
 
 template <int H, int R1, int T1, int SU, int SA, int UNR, int U>
@@ -236,14 +259,14 @@ struct ShiftBlock {
                                                unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
                                                unsigned& mine, float* un, float* lo_peer,
                                                float* hi_peer, const Geo& g, const Coef& K,
-                                               const Ctl& c, const Peer& pr) {
+                                               const Ctl& c, const Peer& pr, const Pub& pub) {
         if (jb + U < it.nq) {
             consumer_step<H, R1, T1, SU, SA, 2 * H + UNR, 2 * H + U>(
                 Q, jb + U, it, ucol, acol, aflag, full_u, empty_u, full_a, empty_a, su, pu, sp, sa, pa_,
-                mine, un, lo_peer, hi_peer, g, K, c, pr);
+                mine, un, lo_peer, hi_peer, g, K, c, pr, pub);
             ShiftBlock<H, R1, T1, SU, SA, UNR, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                            full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                           lo_peer, hi_peer, g, K, c, pr);
+                                                           lo_peer, hi_peer, g, K, c, pr, pub);
         }
     }
 };
@@ -253,12 +276,18 @@ struct ShiftBlock<H, R1, T1, SU, SA, UNR, UNR> {
                                                const float*, const unsigned*, unsigned, unsigned, unsigned,
                                                unsigned, unsigned&, unsigned&, unsigned&, unsigned&,
                                                unsigned&, unsigned&, float*, float*, float*, const Geo&,
-                                               const Coef&, const Ctl&, const Peer&) {}
+                                               const Coef&, const Ctl&, const Peer&, const Pub&) {}
 };
 
-template <int H, int R1, int T1, int SU, int SA, int UNR>
-__global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
-    k_tma(const __grid_constant__ Maps maps, Geo g, Coef K, Ctl c, Peer pr, Sched sc) {
+// The kernel body.  role 0: one time step (K1).  Temporal blocking of two steps (K3) runs
+// two roles in one launch: role 1 CTAs compute u[t+1] (level (s+1)%3) for their item plus H
+// overlap planes on each dim-0 side, publishing per-plane progress; role 2 CTAs compute
+// u[t+2] from it (c.step already advanced by one), their TMA producer waiting on the progress
+// counters of the 3x3 neighbouring stage-1 columns before each u[t+1] plane, and before
+// overwriting u[t-1] planes that a neighbouring chunk's stage 1 still reads.
+template <int H, int R1, int T1, int SU, int SA, int UNR, int TB>
+__device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const Coef& K, const Ctl& c,
+                                         const Peer& pr, const Sched& sc, const TbCtl& tb, int role) {
     using C = Cfg<H, R1, T1>;
     constexpr int NQ = C::NQ;
     // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
@@ -269,6 +298,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     unsigned char* aring = smem + SU * C::UPLANE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(aring + SA * 3 * C::ATILE);
     unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA));  // damp-present per aux stage
+    unsigned* tally = aflag + SA;  // K3: per-plane warp tallies [16]
     const unsigned full_u = smem_addr(bars), empty_u = full_u + 8 * SU;
     const unsigned full_a = empty_u + 8 * SU, empty_a = full_a + 8 * SA;
     const unsigned uring_s = smem_addr(uring), aring_s = smem_addr(aring);
@@ -283,6 +313,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             mbar_init(full_a + 8 * i, 1);
             mbar_init(empty_a + 8 * i, 32 * C::NCW);
         }
+        for (int i = 0; i < 16; ++i) tally[i] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -292,8 +323,21 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     const int lt = c.step % 3, ln = (c.step + 1) % 3, lp = (c.step + 2) % 3;
-    const int G = gridDim.x;
     const int nitems = sc.ncol * sc.nchunk;
+    // K1: persistent CTAs stride over the items; K3: one item per CTA and role.
+    const int first = TB ? static_cast<int>(blockIdx.x) - (role == 2 ? tb.ctas : 0) : static_cast<int>(blockIdx.x);
+    const int G = TB ? tb.ctas : static_cast<int>(gridDim.x);
+    const unsigned long long epoch = TB ? (tb.epoch << 32) : 0ull;
+    if (TB) {
+        // reset this item's stage-1 progress for this launch (after griddepcontrol.wait: the
+        // previous launch's stage-2 CTAs are done polling it), ordered before every
+        // consumer's increments by the CTA barrier
+        if (role == 1 && threadIdx.x == 0) {
+            for (int item = first; item < nitems; item += G) atomicExch(tb.cnt + item, epoch);
+            __threadfence();
+        }
+        __syncthreads();
+    }
     unsigned mine = 0u;
     if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x] = gtimer();
 
@@ -315,16 +359,23 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             unsigned st = 0, ph = 0;
             bool lo_ready = c.ghost_lo_end <= 0 || c.need_lo == 0, hi_ready = !c.flags || c.need_hi == 0;
             if (!c.flags) lo_ready = hi_ready = true;
-            for (int item = blockIdx.x; item < nitems; item += G) {
+            for (int item = first; item < nitems; item += G) {
                 const int col = item % sc.ncol, chunk = item / sc.ncol;
-                const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
-                const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+                int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
+                int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
                 const int dir = (chunk & 1) ? 1 : -1;   // even chunks descend, odd ascend
+                // stage-1 range of a chunk: its planes plus H overlap planes per side
+                const int xa1 = max(xa - H, sc.x0), xb1 = min(xb + H, sc.x0 + sc.np);
+                if (TB && role == 1) {
+                    xa = xa1;
+                    xb = xb1;
+                }
                 const int yt = sc.y0 + (col / sc.nzt) * T1;
                 const int zt = sc.zs + (col % sc.nzt) * kT2;
                 if (lane == 0) {
                     const int q0 = dir > 0 ? xa - H : xb - 1 + H;
                     const int nq = xb - xa + 2 * H;
+                    unsigned long long seen = 0;  // K3 stage 2: min progress seen among neighbours
                     for (int j = 0; j < nq; ++j) {
                         const int q = q0 + dir * j;
                         if (q < c.ghost_lo_end && !lo_ready) {  // lower neighbour's step must be done
@@ -334,6 +385,39 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                         if (q >= c.ghost_hi_begin && !hi_ready) {
                             wait_counter(c.flags + 1, c.need_hi, c.err);
                             hi_ready = true;
+                        }
+                        if (TB && role == 2 && q >= xa1 && q < xb1) {
+                            // u[t+1] plane q (with its y/z halo) must be stored by the stage-1
+                            // CTAs of this column tile and its 3x3 neighbours (same chunk, same
+                            // order); `seen` caches the smallest counter observed so far.
+                            const unsigned long long need =
+                                epoch + static_cast<unsigned long long>(dir > 0 ? q - xa1 + 1 : xb1 - q);
+                            if (seen < need) {
+                                const int cy = col / sc.nzt, cz = col % sc.nzt;
+                                const int ya = max(cy - 1, 0), yb = min(cy + 1, sc.nyt - 1);
+                                const int za = max(cz - 1, 0), zb = min(cz + 1, sc.nzt - 1);
+                                const unsigned long long* base = tb.cnt + chunk * sc.ncol;
+                                const unsigned long long t0 = gtimer();
+                                while (true) {  // all neighbour counters polled concurrently
+                                    unsigned long long lo = ~0ull;
+                                    for (int ny = ya; ny <= yb; ++ny)
+                                        for (int nz = za; nz <= zb; ++nz) {
+                                            unsigned long long v;
+                                            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];"
+                                                         : "=l"(v) : "l"(base + ny * sc.nzt + nz) : "memory");
+                                            lo = v < lo ? v : lo;
+                                        }
+                                    seen = lo;
+                                    if (lo >= need) break;
+                                    if (gtimer() - t0 > 20000000000ull) {
+                                        atomicExch(c.err, 1u);
+                                        break;
+                                    }
+                                    __nanosleep(20);
+                                }
+                                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
+                            }
                         }
                         mbar_wait(empty_u + 8 * st, ph ^ 1u);
                         mbar_expect_tx(full_u + 8 * st, C::ROWS * C::W2 * 4);
@@ -346,6 +430,24 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                     const int p0 = dir > 0 ? xa : xb - 1;
                     for (int j = 0; j < xb - xa; ++j) {
                         const int p = p0 + dir * j;
+                        if (TB && role == 2) {
+                            // u[t+2] overwrites u[t-1]: the neighbouring chunks' stage 1 reads
+                            // u[t-1] on its H overlap planes; it must be past plane p first.
+                            if (chunk > 0 && p < xa + H) {
+                                const int xa0 = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk - 1) / sc.nchunk);
+                                const int pa1 = max(xa0 - H, sc.x0), pb1 = min(xa + H, sc.x0 + sc.np);
+                                const int n = ((chunk - 1) & 1) ? p - pa1 + 1 : pb1 - p;
+                                wait_gpu(tb.cnt + (chunk - 1) * sc.ncol + col, epoch + static_cast<unsigned long long>(n),
+                                         c.err);
+                            }
+                            if (chunk + 1 < sc.nchunk && p >= xb - H) {
+                                const int xb2 = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 2) / sc.nchunk);
+                                const int pa1 = max(xb - H, sc.x0), pb1 = min(xb2 + H, sc.x0 + sc.np);
+                                const int n = ((chunk + 1) & 1) ? p - pa1 + 1 : pb1 - p;
+                                wait_gpu(tb.cnt + (chunk + 1) * sc.ncol + col, epoch + static_cast<unsigned long long>(n),
+                                         c.err);
+                            }
+                        }
                         mbar_wait(empty_a + 8 * st, ph ^ 1u);
                         const unsigned need_damp = (!dfl || dfl[p]) ? 1u : 0u;
                         aflag[st] = need_damp;  // published by the arrive below (release)
@@ -376,11 +478,19 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
         float4 Q[R1][kUnroll ? NQ : 1];   // rotating register queue (H <= 3)
         float4 Qs[R1][kUnroll ? 1 : 2 * H + UNR];  // shifting register queue (H >= 4)
         unsigned su = 0, pu = 0, sp = 0, sa = 0, pa_ = 0;
-        for (int item = blockIdx.x; item < nitems; item += G) {
+        for (int item = first; item < nitems; item += G) {
+            Pub pub;
+            pub.cnt = (TB && role == 1) ? tb.cnt + item : nullptr;
+            pub.base = epoch;
+            pub.done = tally;
             const int col = item % sc.ncol, chunk = item / sc.ncol;
             Item it;
             it.xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
             it.xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+            if (TB && role == 1) {
+                it.xa = max(it.xa - H, sc.x0);
+                it.xb = min(it.xb + H, sc.x0 + sc.np);
+            }
             it.dir = (chunk & 1) ? 1 : -1;
             it.q0 = it.dir > 0 ? it.xa - H : it.xb - 1 + H;
             it.nq = it.xb - it.xa + 2 * H;
@@ -392,7 +502,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
             it.rows_ok = it.yt + R1 - 1 < sc.y1;
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
             sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
-            if (c.trace && ct == 0 && item == blockIdx.x) {
+            if (c.trace && ct == 0 && item == first) {
                 // time when the first output plane's data is complete (end of warm-up)
                 unsigned s2 = (su + 2 * H) % SU, p2 = pu ^ (((su + 2 * H) / SU) & 1u);
                 mbar_wait(full_u + 8 * s2, p2);
@@ -403,7 +513,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                 for (int jb = 0; jb < it.nq; jb += NQ)
                     Unrolled<H, R1, T1, SU, SA, 0>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                         full_a, empty_a, su, pu, sp, sa, pa_, mine,
-                                                        un, lo_peer, hi_peer, g, K, c, pr);
+                                                        un, lo_peer, hi_peer, g, K, c, pr, pub);
             } else {
                 // Partial unroll by UNR with a queue of 2H+UNR slots: plane j-m lives in slot
                 // 2H+u-m inside a block, and the queue shifts down by UNR once per block
@@ -412,7 +522,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
                 for (int jb = 0; jb < it.nq; jb += UNR) {
                     ShiftBlock<H, R1, T1, SU, SA, UNR, 0>::run(Qs, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                              full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                             lo_peer, hi_peer, g, K, c, pr);
+                                                             lo_peer, hi_peer, g, K, c, pr, pub);
 #pragma unroll
                     for (int i = 0; i < R1; ++i)
 #pragma unroll
@@ -430,11 +540,27 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
     if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
 }
 
+template <int H, int R1, int T1, int SU, int SA, int UNR, int TB>
+__global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
+    k_tma(const __grid_constant__ Maps maps, Geo g, Coef K, Ctl c, Peer pr, Sched sc, TbCtl tb) {
+    if constexpr (TB) {
+        const int role = static_cast<int>(blockIdx.x) >= tb.ctas ? 2 : 1;
+        Ctl cc = c;
+        if (role == 2) {  // the second of the two steps
+            ++cc.step;
+            ++cc.slot;
+        }
+        tma_body<H, R1, T1, SU, SA, UNR, 1>(maps, g, K, cc, pr, sc, tb, role);
+    } else {
+        tma_body<H, R1, T1, SU, SA, UNR, 0>(maps, g, K, c, pr, sc, tb, 0);
+    }
+}
+
 template <int H, int R1, int T1, int SU, int SA>
 size_t smem_bytes() {
     using C = Cfg<H, R1, T1>;
     return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
-           16 * (SU + SA) + 4 * SA;
+           16 * (SU + SA) + 4 * SA + 4 * 16;
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
@@ -453,17 +579,19 @@ size_t smem_bytes() {
     X(8, 1, 22, 11, 3, 4)        \
     X(8, 1, 22, 14, 3, 4)
 
-using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
+using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl);
 
 struct Variant {
     int H, R1, T1, SU, SA, UNR;
-    KernelFn fn;
+    KernelFn fn;     // one step per launch (K1)
+    KernelFn fn_tb;  // two steps per launch (K3)
     size_t smem;
     int threads;
 };
 
-#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa, unr) \
-    {h, r1, t1, su, sa, unr, k_tma<h, r1, t1, su, sa, unr>, smem_bytes<h, r1, t1, su, sa>(), Cfg<h, r1, t1>::NTHREADS},
+#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa, unr)                                                     \
+    {h, r1, t1, su, sa, unr, k_tma<h, r1, t1, su, sa, unr, 0>, k_tma<h, r1, t1, su, sa, unr, 1>,   \
+     smem_bytes<h, r1, t1, su, sa>(), Cfg<h, r1, t1>::NTHREADS},
 
 // Rows per consumer thread: R1 = 1 doubles the consumer warps per SM (more latency hiding)
 // at the cost of re-reading the y-neighbour rows per row; SWB_R1=1|2 overrides the default.
@@ -544,6 +672,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     TmaPlan p{};
     p.ok = 0;
     p.H = H;
+    p.num_sms = num_sms;
     const char* env = std::getenv("SWB_KERNEL");
     const bool want_rq = !(env && std::strcmp(env, "sq") == 0);
     int T1 = 0, threads = 0, smem = 0;
@@ -594,9 +723,38 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     }
     p.nchunk = best;
     p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * best));
+    // K3 (two steps per launch): half the SMs run stage 1, half stage 2, all co-resident (the
+    // stage-2 CTAs spin on stage-1 progress).  Stage 1 also computes H overlap planes per
+    // chunk side; chunks are at least H planes long (the overlap only reaches the next chunk).
+    {
+        const int half = num_sms / 2;
+        int tb_best = 0;
+        double tb_cost = 1e300;
+        for (int nc = 1; nc <= 32 && nc * std::max(H, 4) <= np; ++nc) {
+            const long long items = static_cast<long long>(p.columns) * nc;
+            const long long rounds = (items + half - 1) / half;
+            const double len = static_cast<double>(np) / nc;
+            const double cost = static_cast<double>(rounds) * (std::ceil(len) + 0.5 * 2 * H + 2 * H);
+            if (cost < tb_cost - 1e-9) {
+                tb_cost = cost;
+                tb_best = nc;
+            }
+        }
+        p.nchunk_tb = tb_best;
+        p.tb_items = tb_best > 0 ? p.columns * tb_best : 0;
+        p.tb_ok = (p.kind == 0 && tb_best > 0 && half >= 1) ? 1 : 0;
+    }
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return p;
+    }
+    if (p.tb_ok && p.kind == 0) {
+        const Variant* v = find_variant(H);
+        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(v->fn_tb),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+            cudaGetLastError();
+            p.tb_ok = 0;
+        }
     }
     p.ok = 1;
     return p;
@@ -689,8 +847,33 @@ cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, cons
     sc.zs = plan.zs;
     sc.x0 = g.x0;
     if (plan.kind == 1) return launch_sq(plan, maps, g, K, c, p, &sc, s);
+    TbCtl tb{};
     return launch_pdl(reinterpret_cast<const void*>(v->fn), plan.grid, v->threads, v->smem, s,
-                      *static_cast<const Maps*>(maps), g, K, c, p, sc);
+                      *static_cast<const Maps*>(maps), g, K, c, p, sc, tb);
+}
+
+cudaError_t launch_tma_tb(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
+                          const Ctl& c, const TbCtl& tb_in, cudaStream_t s) {
+    const Variant* v = find_variant(plan.H);
+    if (!plan.ok || !plan.tb_ok || plan.kind != 0 || !v || !tb_in.cnt) return cudaErrorInvalidValue;
+    Sched sc;
+    sc.nyt = plan.tiles_y;
+    sc.nzt = plan.tiles_z;
+    sc.ncol = plan.columns;
+    sc.np = g.x1 - g.x0;
+    sc.nchunk = plan.nchunk_tb;
+    sc.dflag = plan.dflag;
+    sc.y0 = g.y0;
+    sc.y1 = g.y1;
+    sc.z0 = g.z0;
+    sc.z1 = g.z1;
+    sc.zs = plan.zs;
+    sc.x0 = g.x0;
+    TbCtl tb = tb_in;
+    tb.ctas = tb_ctas(plan);
+    Peer none{};
+    return launch_pdl(reinterpret_cast<const void*>(v->fn_tb), 2 * tb.ctas, v->threads, v->smem, s,
+                      *static_cast<const Maps*>(maps), g, K, c, none, sc, tb);
 }
 
 }  // namespace swb

@@ -191,6 +191,28 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* flag, uns
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Intra-GPU progress wait (temporal blocking): gpu-scope acquire polls with a short backoff,
+// bounded at ~20 s (then records an error instead of hanging).  Returns the value seen.
+// No proxy fence here: the caller issues one fence.proxy.async after all its waits.
+__device__ __forceinline__ unsigned long long wait_gpu(const unsigned long long* flag, unsigned long long need,
+                                                       unsigned* err) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v < need) {
+        const unsigned long long t0 = gtimer();
+        while (true) {
+            __nanosleep(32);
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+            if (v >= need) break;
+            if (gtimer() - t0 > 20000000000ull) {
+                atomicExch(err, 1u);
+                break;
+            }
+        }
+    }
+    return v;
+}
+
 // End-of-CTA signal for the fused halo exchange (after the CTA barrier in block_max_commit).
 __device__ __forceinline__ void signal_neighbours(const Ctl& c) {
     if (threadIdx.x == 0 && (c.sig_lo || c.sig_hi)) {
@@ -202,9 +224,8 @@ __device__ __forceinline__ void signal_neighbours(const Ctl& c) {
 
 // Launch a stencil kernel with programmatic stream serialization (PDL): the next step's
 // CTAs start their prologue while this step drains; they block in griddepcontrol.wait.
-inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
-                              const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
-                              const Sched& sc) {
+inline cudaError_t launch_pdl_args(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
+                                   void** args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
@@ -215,9 +236,24 @@ inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+// k_sq kernels: (Maps, Geo, Coef, Ctl, Peer, Sched)
+inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
+                              const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
+                              const Sched& sc) {
     void* args[] = {const_cast<Maps*>(&maps), const_cast<Geo*>(&g), const_cast<Coef*>(&K),
                     const_cast<Ctl*>(&c), const_cast<Peer*>(&p), const_cast<Sched*>(&sc)};
-    return cudaLaunchKernelExC(&cfg, fn, args);
+    return launch_pdl_args(fn, grid, threads, smem, s, args);
+}
+// k_tma kernels: (Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl)
+inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
+                              const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
+                              const Sched& sc, const TbCtl& tb) {
+    void* args[] = {const_cast<Maps*>(&maps), const_cast<Geo*>(&g), const_cast<Coef*>(&K),
+                    const_cast<Ctl*>(&c), const_cast<Peer*>(&p), const_cast<Sched*>(&sc),
+                    const_cast<TbCtl*>(&tb)};
+    return launch_pdl_args(fn, grid, threads, smem, s, args);
 }
 
 }  // namespace tma

@@ -6,6 +6,14 @@
 
 namespace swb {
 
+// Temporal blocking (K3, two steps per launch): stage-1 progress counters, one per work item,
+// cumulative within a launch and tagged with the launch epoch in the high 32 bits.
+struct TbCtl {
+    unsigned long long* cnt;  // [items] device counters (null for single-step launches)
+    unsigned long long epoch; // launch sequence number (>= 1)
+    int ctas;                 // CTAs per stage; the grid is 2 * ctas
+};
+
 // One-thread-per-point stencil step; form: 0 factorised, 1 plain FP64, 2 plain FP32.
 cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ctl& c,
                           const Peer& p, cudaStream_t s);
@@ -27,7 +35,15 @@ struct TmaPlan {
     const unsigned char* dflag;  // device [columns][planes] damp-tile-nonzero flags (or null)
     int variant;
     int kind;             // 0: register-queue kernel (k_tma.cu), 1: smem-queue kernel (k_sq.cu)
+    // K3 schedule (two steps per launch): nchunk_tb dim-0 chunks so that 2 x items CTAs are
+    // co-resident (one per SM); tb_ok = 0 if the grid is too small for that.
+    int tb_ok;
+    int nchunk_tb;
+    int tb_items;
+    int num_sms;
 };
+// CTAs per stage of a K3 launch (the grid is twice this).
+inline int tb_ctas(const TmaPlan& p) { return p.tb_items < p.num_sms / 2 ? p.tb_items : p.num_sms / 2; }
 // Host-side damp tile flags for a plan: flags[col * np + (x - x0)] = any damp != 0 in the tile.
 void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_local, int n1, int n2,
                     unsigned char* flags);
@@ -39,6 +55,10 @@ constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps
 cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*kTmaMapsBytes*/);
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s);
+// K3: steps c.step and c.step+1 in one launch (single domain, no linked neighbours); smax
+// slots c.slot and c.slot+1.
+cudaError_t launch_tma_tb(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
+                          const Ctl& c, const TbCtl& tb, cudaStream_t s);
 
 cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
                             int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,

@@ -79,6 +79,8 @@ struct swb_handle {
     alignas(128) unsigned char maps[kTmaMapsBytes];
     bool use_tma = false;
     unsigned char* d_dflag = nullptr;
+    unsigned long long* d_tbcnt = nullptr;  // K3 stage-1 progress counters [plan.tb_items]
+    unsigned long long tb_epoch = 0;         // K3 launches so far (counter tag)
     unsigned long long* d_trace = nullptr;  // SWB_TRACE: per-CTA timestamps of the last launch
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
@@ -180,10 +182,38 @@ int refresh_ring(swb_handle* h) {
     return SWB_OK;
 }
 
+bool linked(const swb_handle* h) { return h->lo_remote || h->hi_remote || h->peer.lo_lev[0] || h->peer.hi_lev[0]; }
+
+// Temporal blocking applies to a single-domain TMA handle (slabs exchange halos every step).
+bool use_tb(const swb_handle* h) { return h->time_block >= 2 && h->use_tma && h->plan.tb_ok && h->d_tbcnt && !linked(h); }
+
 int enqueue_steps(swb_handle* h, int step0, int nt) {
     const int kmask = (h->lo_remote && !h->fused_lo ? 1 : 0) | (h->hi_remote && !h->fused_hi ? 2 : 0);
-    for (int i = 0; i < nt; ++i) {
+    const bool tb = use_tb(h);
+    for (int i = 0; i < nt;) {
         const int s = step0 + i;
+        if (tb && i + 1 < nt) {
+            // K3: steps s and s+1 in one launch, then both steps' receiver samples
+            Ctl c = h->ctl;
+            c.step = s;
+            c.slot = i;
+            c.err = h->d_err;
+            c.ghost_lo_end = 0;
+            c.ghost_hi_begin = INT_MAX;
+            TbCtl t{};
+            t.cnt = h->d_tbcnt;
+            t.epoch = ++h->tb_epoch;
+            SWB_CUDA(launch_tma_tb(h->plan, h->maps, h->geo, h->K, c, t, h->stream));
+            ++h->launches;
+            for (int k = 0; k < 2 && !h->rec_owned.empty(); ++k) {
+                const int owned = static_cast<int>(h->rec_owned.size());
+                SWB_CUDA(launch_samplers(h->u + ((s + k + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w,
+                                         owned, h->d_traces + static_cast<long long>(i + k) * owned, h->stream));
+                ++h->launches;
+            }
+            i += 2;
+            continue;
+        }
         if (kmask) {  // kernel-based ordering for sides without fused support
             SWB_CUDA(launch_wait_flags(h->d_flags, kmask, h->steps_done + i, h->d_err, h->stream));
             ++h->launches;
@@ -228,6 +258,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
                                          h->steps_done + i + 1, h->stream));
             ++h->launches;
         }
+        ++i;
     }
     h->steps_done += nt;
     return SWB_OK;
@@ -280,7 +311,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     if (!(p->dt > 0.0f)) return fail(SWB_EINVAL, "dt must be positive");
     if (!p->m) return fail(SWB_EINVAL, "m (squared slowness) is required");
     if (p->form < 0 || p->form > 4) return fail(SWB_EINVAL, "unknown stencil form");
-    if (p->time_block < 0) return fail(SWB_EINVAL, "time_block must be >= 1");
+    if (p->time_block < 0 || p->time_block > 2)
+        return fail(SWB_EINVAL, "time_block must be 1 (one step per launch) or 2 (temporal blocking)");
     const int HU = p->space_order / 2;
     const int H = std::max(HU, 1);  // widest halo among u (SO/2), m and damp (1): src/pipeline.cpp:79-88
     const char* dn[3] = {"x", "y", "z"};
@@ -493,6 +525,10 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             if (p->damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
             h->plan.dflag = h->d_dflag;
             h->use_tma = true;
+            if (h->time_block >= 2 && h->plan.tb_ok) {
+                SWB_CUDA_C(cudaMalloc(&h->d_tbcnt, sizeof(unsigned long long) * h->plan.tb_items));
+                SWB_CUDA_C(cudaMemsetAsync(h->d_tbcnt, 0, sizeof(unsigned long long) * h->plan.tb_items, h->stream));
+            }
         }
     }
     h->stats.kernel_variant = h->use_tma ? h->plan.variant : 100 + h->form;
@@ -500,7 +536,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         SWB_CUDA_C(cudaMalloc(&h->d_trace, sizeof(unsigned long long) * 4 * 1024));
         h->ctl.trace = h->d_trace;
     }
-    h->stats.launch_steps = 1;
+    h->stats.launch_steps = (h->time_block >= 2 && h->use_tma && h->plan.tb_ok) ? 2 : 1;
+    if (h->stats.launch_steps == 2) h->stats.kernel_variant += 10000;  // K3 (two-step) variant ids
     compute_peer_ranges(h);
     SWB_CUDA_C(cudaStreamSynchronize(h->stream));
     *out = h;
@@ -658,6 +695,7 @@ int swb_destroy(swb_handle* h) {
                     static_cast<void*>(h->d_rec_w),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
                     static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err),
+                    static_cast<void*>(h->d_tbcnt),
                     static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -706,6 +744,7 @@ int swb_link_local(swb_handle* lower, swb_handle* upper) {
     lower->fused_hi = upper->fused_lo = fused;
     lower->nb_grid_hi = upper->plan.grid;
     upper->nb_grid_lo = lower->plan.grid;
+    lower->stats.launch_steps = upper->stats.launch_steps = 1;  // linked slabs step one at a time
     compute_peer_ranges(lower);
     compute_peer_ranges(upper);
     return SWB_OK;
@@ -771,6 +810,7 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         h->fused_hi = b.fused_capable && fused_capable(h);
         h->nb_grid_hi = b.grid;
     }
+    h->stats.launch_steps = 1;  // linked slabs step one at a time
     compute_peer_ranges(h);
     return SWB_OK;
 }

@@ -1,5 +1,5 @@
 """Quick device-time probe of each stencil form at 256^3 (not the bench; for development)."""
-import sys, time
+import os, sys, time
 import numpy as np
 sys.path.insert(0, '.')
 import paper_1912_00695_b200 as P
@@ -12,7 +12,7 @@ for so in sos:
     prob = P.make_wave_problem(P.WaveProblemConfig(shape=(n, n, n), spacing=(10., 10., 10.), space_order=so, steps=nt + 10))
     pts = (n - so) ** 3
     for f in forms:
-        op = P.Operator(prob, form=f)
+        op = P.Operator(prob, form=f, time_block=int(os.environ.get("TB", "1")))
         op.apply(5, 0)
         r = op.apply(nt, 5)
         st = op.stats()
