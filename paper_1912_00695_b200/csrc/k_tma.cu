@@ -44,7 +44,8 @@ using namespace tma;
 struct Pub {
     unsigned long long* cnt;  // this item's global counter (null: not publishing)
     unsigned long long base;  // epoch tag
-    unsigned* done;           // smem [16] per-plane warp tallies
+    unsigned* done;           // smem [16] per-plane warp tallies, [16] = (seq << 16) | planes complete
+    unsigned seq;             // this CTA's item sequence number (tags `complete`)
 };
 
 template <int H, int R1, int T1, int SU, int SA, int QN, int U>
@@ -207,14 +208,37 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
     // Temporal blocking, stage 1: publish "this warp has stored one more u[t+1] plane"
     // (the stage-2 CTAs wait on these counters before reading the plane through TMA).
     if (pub.cnt) {
-        __syncwarp();
+        // A plane is done when its last warp tallies it; that warp records it in `complete`
+        // (CTA scope).  The gpu-scope release (fence + red.max) is paid by the FIRST warp to
+        // finish a later plane -- a warp that is ahead of the others, so the fence does not
+        // stall the slowest warp (which gates the whole CTA through the rings).  The item's
+        // final plane is published by its last warp.
+        __syncwarp();  // orders the warp's stores before lane 0's tally (bar.warp.sync)
         if ((threadIdx.x & 31) == 0) {
-            __threadfence();  // this warp's stores (seen through __syncwarp) before the tally
             const int n = j - 2 * H;  // output plane index within the item
-            const unsigned old = atomicAdd(pub.done + (n & 15), 1u);
-            if (old == C::NCW - 1) {  // last warp for this plane: publish
+            unsigned old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old) : "r"(smem_addr(pub.done + (n & 15))) : "memory");
+            const unsigned tag = pub.seq << 16;
+            if (old == C::NCW - 1) {  // last warp for plane n
                 pub.done[n & 15] = 0u;
-                atomicMax(pub.cnt, pub.base + static_cast<unsigned long long>(n + 1));
+                asm volatile("red.release.cta.shared::cta.max.u32 [%0], %1;"
+                             :: "r"(smem_addr(pub.done + 16)), "r"(tag | static_cast<unsigned>(n + 1)) : "memory");
+                if (n + 1 == it.xb - it.xa) {  // the item's final plane
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
+                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(n + 1)) : "memory");
+                }
+            } else if (old == 0u && n > 0) {  // first warp for plane n: publish what is complete
+                unsigned done_;
+                asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                             : "=r"(done_) : "r"(smem_addr(pub.done + 16)) : "memory");
+                if ((done_ & ~0xffffu) == tag && (done_ & 0xffffu) != 0u) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
+                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(done_ & 0xffffu))
+                                 : "memory");
+                }
             }
         }
     }
@@ -298,7 +322,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     unsigned char* aring = smem + SU * C::UPLANE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(aring + SA * 3 * C::ATILE);
     unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA));  // damp-present per aux stage
-    unsigned* tally = aflag + SA;  // K3: per-plane warp tallies [16]
+    unsigned* tally = aflag + SA;  // K3: per-plane warp tallies [16] + complete-plane word
     const unsigned full_u = smem_addr(bars), empty_u = full_u + 8 * SU;
     const unsigned full_a = empty_u + 8 * SU, empty_a = full_a + 8 * SA;
     const unsigned uring_s = smem_addr(uring), aring_s = smem_addr(aring);
@@ -313,7 +337,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             mbar_init(full_a + 8 * i, 1);
             mbar_init(empty_a + 8 * i, 32 * C::NCW);
         }
-        for (int i = 0; i < 16; ++i) tally[i] = 0u;
+        for (int i = 0; i < 17; ++i) tally[i] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -413,7 +437,6 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                                         atomicExch(c.err, 1u);
                                         break;
                                     }
-                                    __nanosleep(20);
                                 }
                                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
                                 asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -483,6 +506,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             pub.cnt = (TB && role == 1) ? tb.cnt + item : nullptr;
             pub.base = epoch;
             pub.done = tally;
+            pub.seq = static_cast<unsigned>((item - first) / G + 1);
             const int col = item % sc.ncol, chunk = item / sc.ncol;
             Item it;
             it.xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
@@ -560,7 +584,7 @@ template <int H, int R1, int T1, int SU, int SA>
 size_t smem_bytes() {
     using C = Cfg<H, R1, T1>;
     return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
-           16 * (SU + SA) + 4 * SA + 4 * 16;
+           16 * (SU + SA) + 4 * SA + 4 * 17;
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.

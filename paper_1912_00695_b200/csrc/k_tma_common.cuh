@@ -201,7 +201,6 @@ __device__ __forceinline__ unsigned long long wait_gpu(const unsigned long long*
     if (v < need) {
         const unsigned long long t0 = gtimer();
         while (true) {
-            __nanosleep(32);
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
             if (v >= need) break;
             if (gtimer() - t0 > 20000000000ull) {
