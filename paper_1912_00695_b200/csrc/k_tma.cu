@@ -745,6 +745,10 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
             best = nc;
         }
     }
+    if (const char* env_nc = std::getenv("SWB_NCHUNK")) {  // development override
+        const int v = std::atoi(env_nc);
+        if (v >= 1 && v <= np) best = v;
+    }
     p.nchunk = best;
     p.grid = static_cast<int>(std::min<long long>(num_sms, static_cast<long long>(p.columns) * best));
     // K3 (two steps per launch): half the SMs run stage 1, half stage 2, all co-resident (the
