@@ -38,6 +38,11 @@ namespace swb {
 namespace {
 using namespace tma;
 
+#ifndef SWB_TB_LEAD
+#define SWB_TB_LEAD 4
+#endif
+constexpr int kTbLead = SWB_TB_LEAD;  // K3: planes stage 1 must be ahead of stage 2's request
+
 // K3 stage-1 progress publication: a plane counts as done once every consumer warp has
 // stored its rows of it (warps drift apart by up to SU-H planes, so a per-plane smem tally
 // over a ring of 16 slots finds the last warp, which publishes with atomicMax).
@@ -414,9 +419,14 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                             // u[t+1] plane q (with its y/z halo) must be stored by the stage-1
                             // CTAs of this column tile and its 3x3 neighbours (same chunk, same
                             // order); `seen` caches the smallest counter observed so far.
+                            // Ask for kTbLead planes more than needed (capped at the stage-1
+                            // item's end): stage 2 then trails stage 1 by a few planes instead of
+                            // running dry at its edge, so its TMA ring stays primed.
+                            const int idx = dir > 0 ? q - xa1 + 1 : xb1 - q;
+                            const unsigned long long need_min = epoch + static_cast<unsigned long long>(idx);
                             const unsigned long long need =
-                                epoch + static_cast<unsigned long long>(dir > 0 ? q - xa1 + 1 : xb1 - q);
-                            if (seen < need) {
+                                epoch + static_cast<unsigned long long>(min(idx + kTbLead, xb1 - xa1));
+                            if (seen < need_min) {
                                 const int cy = col / sc.nzt, cz = col % sc.nzt;
                                 const int ya = max(cy - 1, 0), yb = min(cy + 1, sc.nyt - 1);
                                 const int za = max(cz - 1, 0), zb = min(cz + 1, sc.nzt - 1);
@@ -437,6 +447,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                                         atomicExch(c.err, 1u);
                                         break;
                                     }
+                                    __nanosleep(64);
                                 }
                                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
                                 asm volatile("fence.proxy.async.global;" ::: "memory");
