@@ -125,6 +125,20 @@ int swb_get_level(swb_handle* h, int level, float* grid_sized);
 int swb_apply(swb_handle* h, int step0, int nt, float* step_max_abs, int32_t* first_bad_step,
               float* rec_traces);
 
+/* Adjoint operator (new; the reference has none -- PAPER.md:350 lists adjoint/RTM as future
+ * work).  The forward map of swb_apply from the source wavelet w to the receiver traces d is
+ * linear: D u[n+1] = (2M + dt^2 L) u[n] - E u[n-1] + S w[n], d[n] = R u[n+1] with
+ * D = m + damp dt/2, E = m - damp dt/2, S = e_s dt^2/m_s.  Its transpose is the same stencil run
+ * backwards in time: starting from zero, for k = nt..1
+ *     z[k] = stencil(z[k+1], z[k+2]) + D^-1 R^T rec_data[k-1],
+ *     src_trace[k-1] = dt^2 (m_s + g_s)/m_s * z[k][source],
+ * with the handle's receivers (on-grid and trilinear) as injection points.  rec_data is
+ * [nt][n_receivers + n_coord_receivers]; the handle's levels are overwritten (zeroed first).
+ * Single-domain handles only.  step_max_abs / first_bad_step as in swb_apply (adjoint-step order).
+ * Restated on the CPU by oracle/port/wave_port.c port_adjoint (tests/test_oracle_adjoint.py). */
+int swb_apply_adjoint(swb_handle* h, int nt, const float* rec_data, float* src_trace, float* step_max_abs,
+                      int32_t* first_bad_step);
+
 /* Asynchronous halves of swb_apply for callers that time on the device: enqueue the time
  * loop on the handle's stream, then collect the same outputs. */
 int swb_apply_async(swb_handle* h, int step0, int nt);

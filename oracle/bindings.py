@@ -268,3 +268,25 @@ def ref_emit_c(cfg: OracleConfig, dse: str = "basic") -> str:
 def omp_threads(which: str = "port") -> int:
     lib = _lib(which)
     return int(getattr(lib, ("ref_" if which == "ref" else "port_") + "omp_max_threads")())
+
+
+def port_adjoint(cfg: OracleConfig, rec_data: np.ndarray, *, receivers=None, receiver_coords=None,
+                 threads: int = 0) -> np.ndarray:
+    """Adjoint of the C restatement's forward map (source wavelet -> receiver traces): the
+    receiver data rec_data[steps][n_rec + n_coord] is injected backwards in time and the
+    source-point trace [steps] is returned (see port_adjoint in port/wave_port.c)."""
+    lib = _lib("port")
+    c = cfg.to_c()
+    rec = None if receivers is None else np.ascontiguousarray(receivers, np.int32).reshape(-1, 3)
+    n_rec = 0 if rec is None else rec.shape[0]
+    crec = None if receiver_coords is None else np.ascontiguousarray(receiver_coords, np.float64).reshape(-1, 3)
+    n_crec = 0 if crec is None else crec.shape[0]
+    data = np.ascontiguousarray(rec_data, np.float32).reshape(cfg.steps, n_rec + n_crec)
+    out = np.zeros(cfg.steps, np.float32)
+    rc = lib.port_adjoint(C.byref(c), int(threads), n_rec,
+                          rec.ctypes.data_as(C.POINTER(C.c_int32)) if n_rec else C.POINTER(C.c_int32)(),
+                          n_crec, crec.ctypes.data_as(C.POINTER(C.c_double)) if n_crec else C.POINTER(C.c_double)(),
+                          _fptr(data), _fptr(out))
+    if rc != 0:
+        raise OracleError(rc, lib.port_last_error().decode())
+    return out

@@ -400,6 +400,85 @@ int port_run2(const port_config* c, int threads, const float* const* initial_u, 
     return 0;
 }
 
+/* Adjoint of the forward operator above, restated (an addition: the reference has no adjoint;
+ * PAPER.md:350 lists it as future work).  The forward map is w -> d with
+ *   D u[n+1] = (2M + dt^2 L) u[n] - E u[n-1]  (+ S w[n] after the stencil),  d[n] = R u[n+1],
+ * D = m + damp*dt/2, E = m - damp*dt/2, S = e_s dt^2/m_s, R = receiver sampling (on-grid or
+ * trilinear).  L is symmetric on the interior (zero ring), so the transpose of the block
+ * lower-triangular time-stepping system is the same recurrence run backwards in time:
+ *   z[k] = stencil(z[k+1], z[k+2]) + D^{-1} R^T d[k-1],   (F^T d)[k-1] = (dt^2 (m_s+g_s)/m_s) z[k][s]
+ * for k = nt .. 1 from z = 0.  R^T only reaches interior points: the ring of width SO/2 is never
+ * written by the forward operator, so receivers (or trilinear corners) there have no adjoint.  Step s' = nt-k uses the forward level rotation; the stencil is the
+ * basic form (point_update).  rec_data is [steps][n_rec + n_crec]; src_trace is [steps]. */
+int port_adjoint(const port_config* c, int threads, int n_rec, const int32_t* rec, int n_crec,
+                 const double* crec, const float* rec_data, float* src_trace) {
+    port_problem p;
+    int rc = port_make(c, &p);
+    if (rc) return rc;
+    const int n0 = p.n0, n1 = p.n1, n2 = p.n2, H = p.H;
+    const size_t n = (size_t)n0 * n1 * n2, s0 = (size_t)n1 * n2, s1 = (size_t)n2;
+    const int nr = n_rec + (n_crec > 0 ? n_crec : 0);
+    if (!c->with_source) { port_free(&p); strcpy(g_err, "the adjoint samples at the source point"); return 1; }
+    size_t* ridx = (size_t*)malloc(sizeof(size_t) * 8 * (size_t)(nr > 0 ? nr : 1));
+    double* rw = (double*)malloc(sizeof(double) * 8 * (size_t)(nr > 0 ? nr : 1));
+    int* ncorner = (int*)malloc(sizeof(int) * (size_t)(nr > 0 ? nr : 1));
+    for (int r = 0; r < n_rec; ++r) {
+        ridx[8 * r] = (size_t)rec[3 * r] * s0 + (size_t)rec[3 * r + 1] * s1 + (size_t)rec[3 * r + 2];
+        rw[8 * r] = 1.0;
+        ncorner[r] = 1;
+    }
+    for (int r = 0; r < n_crec; ++r) {
+        if (crec_stencil(&p, crec + 3 * r, ridx + 8 * (n_rec + r), rw + 8 * (n_rec + r))) {
+            free(ridx); free(rw); free(ncorner); port_free(&p);
+            snprintf(g_err, sizeof g_err, "receiver coordinate %d lies outside the grid", r);
+            return 1;
+        }
+        ncorner[n_rec + r] = 8;
+    }
+    if (threads <= 0) {
+#ifdef _OPENMP
+        threads = omp_get_max_threads();
+#else
+        threads = 1;
+#endif
+    }
+    const double dt = (double)p.dt;
+    const size_t si = (size_t)p.src[0] * s0 + (size_t)p.src[1] * s1 + (size_t)p.src[2];
+    const double ws = ((dt * dt) * ((double)p.m[si] + 0.5 * (double)p.damp[si] * dt)) / (double)p.m[si];
+    float* z = (float*)calloc(3 * n, sizeof(float));
+    for (int sp = 0; sp < p.steps; ++sp) {
+        const int k = p.steps - sp;
+        float* zn = z + n * ((sp + 1) % 3);
+        const float* zc = z + n * (sp % 3);
+        const float* zp = z + n * ((sp + 2) % 3);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(threads)
+#endif
+        for (int x = H; x <= n0 - 1 - H; ++x)
+            for (int y = H; y <= n1 - 1 - H; ++y)
+                for (int zz = H; zz <= n2 - 1 - H; ++zz) {
+                    size_t idx = (size_t)x * s0 + (size_t)y * s1 + (size_t)zz;
+                    zn[idx] = point_update(&p, zc, zp, idx, s0, s1, (double)p.m[idx], (double)p.damp[idx]);
+                }
+        const float* drow = rec_data + (size_t)(k - 1) * nr;
+        for (int r = 0; r < nr; ++r)
+            for (int q = 0; q < ncorner[r]; ++q) {
+                const size_t j = ridx[8 * r + q];
+                /* points outside the update interior are never written by the forward
+                 * operator (the ring keeps its values), so they carry no adjoint */
+                const int jx = (int)(j / s0), jy = (int)((j / s1) % (size_t)n1), jz = (int)(j % s1);
+                if (jx < H || jx > n0 - 1 - H || jy < H || jy > n1 - 1 - H || jz < H || jz > n2 - 1 - H)
+                    continue;
+                const double den = (double)p.m[j] + 0.5 * (double)p.damp[j] * dt;
+                zn[j] = (float)((double)zn[j] + (rw[8 * r + q] * (double)drow[r]) / den);
+            }
+        src_trace[k - 1] = (float)(ws * (double)zn[si]);
+    }
+    free(z); free(ridx); free(rw); free(ncorner);
+    port_free(&p);
+    return 0;
+}
+
 int port_omp_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -138,6 +138,36 @@ __global__ void k_samplers(const float* __restrict__ un, const long long* __rest
     }
 }
 
+// Adjoint of the receiver sampling: spread each receiver's datum onto its corners with the
+// weights w (trilinear weight / (m + damp dt/2), zero outside the update interior).
+__global__ void k_inject(float* __restrict__ un, const long long* __restrict__ idx, const double* __restrict__ w,
+                         int n, const float* __restrict__ data) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const double d = static_cast<double>(data[r]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const long long j = idx[8 * r + c];
+        const double wc = w[8 * r + c];
+        if (j < 0 || wc == 0.0) continue;
+        const double inc = __dmul_rn(wc, d);
+        unsigned* a = reinterpret_cast<unsigned*>(un + j);
+        unsigned old = *a, assumed;
+        do {
+            assumed = old;
+            const float nv = static_cast<float>(__dadd_rn(static_cast<double>(__uint_as_float(assumed)), inc));
+            old = atomicCAS(a, assumed, __float_as_uint(nv));
+        } while (old != assumed);
+    }
+}
+
+cudaError_t launch_inject(float* un, const long long* idx, const double* w, int n, const float* data,
+                          cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_inject<<<ceil_div(n, 128), 128, 0, s>>>(un, idx, w, n, data);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
                             cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

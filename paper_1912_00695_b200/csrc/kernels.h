@@ -67,6 +67,10 @@ cudaError_t launch_receivers(const float* un, const long long* idx, int n, float
                              cudaStream_t s);
 cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
                             cudaStream_t s);
+// Adjoint receiver injection: un[idx] += w * data[r] (8 corners per receiver, one rounding of the
+// double sum per corner, CAS loop so coinciding corners accumulate).
+cudaError_t launch_inject(float* un, const long long* idx, const double* w, int n, const float* data,
+                          cudaStream_t s);
 cudaError_t launch_wait_flags(const unsigned long long* flags, int mask,
                               unsigned long long need, unsigned* err, cudaStream_t s);
 cudaError_t launch_signal_flags(unsigned long long* lo_flag, unsigned long long* hi_flag,

@@ -70,6 +70,14 @@ struct swb_handle {
     double* d_rec_w = nullptr;           // [owned][8] corner weights
     float* d_traces = nullptr;
     int traces_cap = 0;
+    // adjoint: per owned receiver corner, w_c / (m + damp dt/2) (0 outside the update interior),
+    // and the source-point sampling stencil (index + dt^2 (m_s + g_s) / m_s)
+    double* d_inj_w = nullptr;
+    long long* d_src_idx = nullptr;
+    double* d_src_w = nullptr;
+    float* d_adj = nullptr;        // [nt][owned] receiver data of the running adjoint
+    float* d_src_trace = nullptr;  // [nt]
+    int adj_cap = 0;
     // stencil
     Geo geo{};
     Coef K{};
@@ -504,12 +512,44 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         }
     }
     if (!ridx.empty()) {
+        // adjoint injection weights (swb_apply_adjoint): D^{-1} R^T restricted to the update
+        // interior (the forward operator never writes the ring, so it has no adjoint there)
+        std::vector<double> iw(rw.size(), 0.0);
+        const double dtd = static_cast<double>(p->dt);
+        const int Hh = H;
+        for (size_t q = 0; q < ridx.size(); ++q) {
+            if (ridx[q] < 0) continue;
+            const long long j = ridx[q];
+            const int lx = static_cast<int>(j / h->plane) + h->xg_off;
+            const int y = static_cast<int>((j % h->plane) / h->P2), z = static_cast<int>(j % h->P2);
+            if (lx < Hh || lx > h->n0 - 1 - Hh || y < Hh || y > h->n1 - 1 - Hh || z < Hh || z > h->n2 - 1 - Hh)
+                continue;
+            const size_t gi = (static_cast<size_t>(lx) * h->n1 + y) * h->n2 + z;
+            const double mm = p->m[gi], dd = p->damp ? p->damp[gi] : 0.0;
+            iw[q] = rw[q] / (mm + 0.5 * dd * dtd);
+        }
+        SWB_CUDA_C(cudaMalloc(&h->d_inj_w, sizeof(double) * iw.size()));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_inj_w, iw.data(), sizeof(double) * iw.size(), cudaMemcpyHostToDevice,
+                                   h->stream));
         SWB_CUDA_C(cudaMalloc(&h->d_rec_idx, sizeof(long long) * ridx.size()));
         SWB_CUDA_C(cudaMalloc(&h->d_rec_w, sizeof(double) * rw.size()));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_idx, ridx.data(), sizeof(long long) * ridx.size(),
                                    cudaMemcpyHostToDevice, h->stream));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_w, rw.data(), sizeof(double) * rw.size(), cudaMemcpyHostToDevice,
                                    h->stream));
+    }
+    // Adjoint output sampler at the source point (owned slab only).
+    if (c.has_src) {
+        const size_t gi = (static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2];
+        const double mm = p->m[gi], dd = p->damp ? p->damp[gi] : 0.0, dtd = static_cast<double>(p->dt);
+        std::vector<long long> si(8, -1);
+        std::vector<double> sw(8, 0.0);
+        si[0] = local_index(p->source[0], p->source[1], p->source[2]);
+        sw[0] = ((dtd * dtd) * (mm + 0.5 * dd * dtd)) / mm;
+        SWB_CUDA_C(cudaMalloc(&h->d_src_idx, sizeof(long long) * 8));
+        SWB_CUDA_C(cudaMalloc(&h->d_src_w, sizeof(double) * 8));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_src_idx, si.data(), sizeof(long long) * 8, cudaMemcpyHostToDevice, h->stream));
+        SWB_CUDA_C(cudaMemcpyAsync(h->d_src_w, sw.data(), sizeof(double) * 8, cudaMemcpyHostToDevice, h->stream));
     }
     // Kernel choice: the TMA 2.5D kernel for the factorised form when the plan fits.
     if (h->form == SWB_FORM_FACTORISED) {
@@ -664,6 +704,101 @@ int swb_apply(swb_handle* h, int step0, int nt, float* step_max_abs, int32_t* fi
     return swb_collect(h, step_max_abs, first_bad_step, rec_traces);
 }
 
+int swb_apply_adjoint(swb_handle* h, int nt, const float* rec_data, float* src_trace, float* step_max_abs,
+                      int32_t* first_bad_step) {
+    if (!h) return fail(SWB_EINVAL, "null handle");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is pending");
+    if (nt < 0) return fail(SWB_EINVAL, "steps must be non-negative");
+    if (linked(h)) return fail(SWB_EINVAL, "the adjoint runs on a single-domain handle (not on linked slabs)");
+    if (!h->ctl.has_src || !h->d_src_idx) return fail(SWB_EINVAL, "the adjoint samples at the source point: the problem needs a source");
+    if (h->n_rec <= 0 || !rec_data) return fail(SWB_EINVAL, "the adjoint injects receiver data: receivers are required");
+    SWB_CUDA(cudaSetDevice(h->device));
+    const int owned = static_cast<int>(h->rec_owned.size());
+    if (nt > h->adj_cap) {
+        if (h->d_adj) cudaFree(h->d_adj);
+        if (h->d_src_trace) cudaFree(h->d_src_trace);
+        h->d_adj = nullptr;
+        h->d_src_trace = nullptr;
+        SWB_CUDA(cudaMalloc(&h->d_adj, sizeof(float) * static_cast<size_t>(std::max(nt, 1)) * std::max(owned, 1)));
+        SWB_CUDA(cudaMalloc(&h->d_src_trace, sizeof(float) * static_cast<size_t>(std::max(nt, 1))));
+        h->adj_cap = nt;
+    }
+    int rc = ensure_smax(h, nt);
+    if (rc) return rc;
+    {
+        std::vector<float> gathered(static_cast<size_t>(nt) * owned);
+        for (int i = 0; i < nt; ++i)
+            for (int r = 0; r < owned; ++r)
+                gathered[static_cast<size_t>(i) * owned + r] = rec_data[static_cast<size_t>(i) * h->n_rec + h->rec_owned[r]];
+        if (!gathered.empty())
+            SWB_CUDA(cudaMemcpyAsync(h->d_adj, gathered.data(), sizeof(float) * gathered.size(),
+                                     cudaMemcpyHostToDevice, h->stream));
+        // adjoint state starts at zero (all levels, ring included)
+        SWB_CUDA(cudaMemsetAsync(h->u, 0, sizeof(float) * 3 * h->level_floats, h->stream));
+        SWB_CUDA(cudaMemsetAsync(h->d_ring, 0, 3 * sizeof(unsigned), h->stream));
+        h->ring_dirty = false;
+        if (nt > 0) SWB_CUDA(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned) * nt, h->stream));
+        h->ctl.smax = h->d_smax;
+        h->launches = 0;
+        SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+        for (int sp = 0; sp < nt; ++sp) {
+            const int k = nt - sp;  // z[k] = stencil(z[k+1], z[k+2]) + D^-1 R^T d[k-1]
+            Ctl c = h->ctl;
+            c.has_src = 0;
+            c.step = sp;
+            c.slot = sp;
+            c.err = h->d_err;
+            c.ghost_lo_end = 0;
+            c.ghost_hi_begin = INT_MAX;
+            if (h->use_tma) {
+                SWB_CUDA(launch_tma(h->plan, h->maps, h->geo, h->K, c, h->peer, h->stream));
+            } else {
+                const int form = h->form == SWB_FORM_PLAIN_F64   ? 1
+                                 : h->form == SWB_FORM_PLAIN_F32 ? 2
+                                 : h->form == SWB_FORM_FACTORISED_SIMPLE_F32C ? 3
+                                                                         : 0;
+                SWB_CUDA(launch_simple(h->H, form, h->geo, h->K, c, h->peer, h->stream));
+            }
+            float* un = h->u + ((sp + 1) % 3) * h->level_floats;
+            SWB_CUDA(launch_inject(un, h->d_rec_idx, h->d_inj_w, owned, h->d_adj + static_cast<size_t>(k - 1) * owned,
+                                   h->stream));
+            SWB_CUDA(launch_samplers(un, h->d_src_idx, h->d_src_w, 1, h->d_src_trace + (k - 1), h->stream));
+            h->launches += 3;
+        }
+        SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+    }
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    h->stats.device_ms = ms;
+    h->stats.kernel_launches = h->launches;
+    h->ring_dirty = true;
+    unsigned herr = 0;
+    SWB_CUDA(cudaMemcpy(&herr, h->d_err, sizeof herr, cudaMemcpyDeviceToHost));
+    if (herr) {
+        cudaMemset(h->d_err, 0, sizeof herr);
+        return fail(SWB_ECUDA, "device wait timed out");
+    }
+    std::vector<unsigned> smax(static_cast<size_t>(nt));
+    if (nt > 0) SWB_CUDA(cudaMemcpy(smax.data(), h->d_smax, sizeof(unsigned) * nt, cudaMemcpyDeviceToHost));
+    if (src_trace && nt > 0)
+        SWB_CUDA(cudaMemcpy(src_trace, h->d_src_trace, sizeof(float) * nt, cudaMemcpyDeviceToHost));
+    int bad = -1;
+    for (int i = 0; i < nt; ++i) {
+        float v;
+        if (smax[i] >= 0x7f800000u) {
+            v = std::nanf("");
+            if (bad < 0) bad = i;
+        } else {
+            std::memcpy(&v, &smax[i], sizeof v);
+        }
+        if (step_max_abs) step_max_abs[i] = v;
+    }
+    if (first_bad_step) *first_bad_step = bad;
+    if (bad >= 0) return fail(SWB_EUNSTABLE, "non-finite adjoint field at adjoint step " + std::to_string(bad));
+    return SWB_OK;
+}
+
 void* swb_stream(swb_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
 // Debug (SWB_TRACE=1): copy the per-CTA timestamps of the last stencil launch.
@@ -695,7 +830,9 @@ int swb_destroy(swb_handle* h) {
                     static_cast<void*>(h->d_rec_w),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
                     static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err),
-                    static_cast<void*>(h->d_tbcnt),
+                    static_cast<void*>(h->d_tbcnt), static_cast<void*>(h->d_inj_w),
+                    static_cast<void*>(h->d_src_idx), static_cast<void*>(h->d_src_w),
+                    static_cast<void*>(h->d_adj), static_cast<void*>(h->d_src_trace),
                     static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);

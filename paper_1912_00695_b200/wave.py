@@ -412,6 +412,26 @@ class Operator:
         return RunResult(Field(self.problem), smax, wall, 0, (step0 + nt) % 3, traces,
                          st.device_ms * 1e-3)
 
+    def apply_adjoint(self, rec_data: np.ndarray) -> np.ndarray:
+        """Adjoint of the map source wavelet -> receiver traces (an addition; the reference has
+        no adjoint): inject ``rec_data[nt][n_receivers]`` (on-grid receivers
+        first, then ``receiver_coords``) backwards in time from a zero field and return the
+        source-point trace ``[nt]`` such that <apply traces, rec_data> == <wavelet, result>.
+        Overwrites the operator's levels.  See swb_apply_adjoint in include/swb.h."""
+        n_rec = (0 if self.receivers is None else self.receivers.shape[0]) + \
+            (0 if self.receiver_coords is None else self.receiver_coords.shape[0])
+        data = np.ascontiguousarray(rec_data, np.float32)
+        if data.ndim != 2 or data.shape[1] != n_rec:
+            raise ValueError(f"rec_data must be [nt][{n_rec}]")
+        nt = data.shape[0]
+        out = np.zeros(nt, np.float32)
+        smax = np.zeros(nt, np.float32)
+        bad = C.c_int32(-1)
+        rc = N.lib.swb_apply_adjoint(self._h, nt, N.fptr(data), N.fptr(out), N.fptr(smax), C.byref(bad))
+        if rc != N.SWB_OK:
+            _check(rc, bad.value)
+        return out
+
     def apply_async(self, nt: int, step0: int) -> None:
         _check(N.lib.swb_apply_async(self._h, int(step0), int(nt)))
         self.step = step0 + nt
