@@ -139,6 +139,17 @@ int swb_apply(swb_handle* h, int step0, int nt, float* step_max_abs, int32_t* fi
 int swb_apply_adjoint(swb_handle* h, int nt, const float* rec_data, float* src_trace, float* step_max_abs,
                       int32_t* first_bad_step);
 
+/* swb_apply plus wavefield snapshots (the reference's route is
+ * RunOptions::on_step + write_snapshot, src/executor.cpp:595-596, 816-837, which costs a full
+ * synchronous download per step).  After every `every` steps the newest level is copied
+ * device-to-device into a staging ring in HBM (the compute stream only waits for that copy,
+ * and only before the step that would overwrite the level) and drained to snaps[i]
+ * (grid-sized, reference interior layout; pinned memory for full PCIe speed) on a separate
+ * copy stream, overlapping the following steps.  n_snaps must equal nt / every; snapshot i is
+ * the state after step step0 + (i+1)*every - 1.  Other outputs as swb_apply. */
+int swb_apply_snapshots(swb_handle* h, int step0, int nt, int every, float* const* snaps, int n_snaps,
+                        float* step_max_abs, int32_t* first_bad_step, float* rec_traces);
+
 /* Asynchronous halves of swb_apply for callers that time on the device: enqueue the time
  * loop on the handle's stream, then collect the same outputs. */
 int swb_apply_async(swb_handle* h, int step0, int nt);

@@ -56,6 +56,7 @@ def _load() -> C.CDLL:
         "swb_apply": (C.c_int, [h, C.c_int, C.c_int, fp, P(C.c_int32), fp]),
         "swb_apply_async": (C.c_int, [h, C.c_int, C.c_int]),
         "swb_apply_adjoint": (C.c_int, [h, C.c_int, fp, fp, fp, P(C.c_int32)]),
+        "swb_apply_snapshots": (C.c_int, [h, C.c_int, C.c_int, C.c_int, P(fp), C.c_int, fp, P(C.c_int32), fp]),
         "swb_collect": (C.c_int, [h, fp, P(C.c_int32), fp]),
         "swb_stream": (C.c_void_p, [h]),
         "swb_get_stats": (C.c_int, [h, P(SwbStats)]),
@@ -83,6 +84,7 @@ lib = _load()
 
 # C-ABI entry points declared in include/swb.h (checked by tests/test_capi_symbols.py).
 EXPORTED = ["swb_create", "swb_set_level", "swb_get_level", "swb_apply", "swb_apply_async", "swb_apply_adjoint",
+            "swb_apply_snapshots",
             "swb_collect", "swb_stream", "swb_get_stats", "swb_destroy", "swb_last_error",
             "swb_export_ghosts", "swb_link_neighbours", "swb_link_local", "swb_fd_weights",
             "swb_cfl_dt", "swb_ricker_wavelet", "swb_m_data", "swb_damp_data", "swb_version",

@@ -78,6 +78,11 @@ struct swb_handle {
     float* d_adj = nullptr;        // [nt][owned] receiver data of the running adjoint
     float* d_src_trace = nullptr;  // [nt]
     int adj_cap = 0;
+    // snapshots (swb_apply_snapshots): device staging ring + two copy streams
+    static constexpr int kSnapSlots = 2;
+    float* d_stage[kSnapSlots] = {nullptr, nullptr};
+    cudaStream_t s_d2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_step = nullptr, ev_d2d[kSnapSlots] = {nullptr, nullptr}, ev_d2h[kSnapSlots] = {nullptr, nullptr};
     // stencil
     Geo geo{};
     Coef K{};
@@ -195,7 +200,7 @@ bool linked(const swb_handle* h) { return h->lo_remote || h->hi_remote || h->pee
 // Temporal blocking applies to a single-domain TMA handle (slabs exchange halos every step).
 bool use_tb(const swb_handle* h) { return h->time_block >= 2 && h->use_tma && h->plan.tb_ok && h->d_tbcnt && !linked(h); }
 
-int enqueue_steps(swb_handle* h, int step0, int nt) {
+int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
     const int kmask = (h->lo_remote && !h->fused_lo ? 1 : 0) | (h->hi_remote && !h->fused_hi ? 2 : 0);
     const bool tb = use_tb(h);
     for (int i = 0; i < nt;) {
@@ -204,7 +209,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
             // K3: steps s and s+1 in one launch, then both steps' receiver samples
             Ctl c = h->ctl;
             c.step = s;
-            c.slot = i;
+            c.slot = slot0 + i;
             c.err = h->d_err;
             c.ghost_lo_end = 0;
             c.ghost_hi_begin = INT_MAX;
@@ -216,7 +221,8 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
             for (int k = 0; k < 2 && !h->rec_owned.empty(); ++k) {
                 const int owned = static_cast<int>(h->rec_owned.size());
                 SWB_CUDA(launch_samplers(h->u + ((s + k + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w,
-                                         owned, h->d_traces + static_cast<long long>(i + k) * owned, h->stream));
+                                         owned, h->d_traces + static_cast<long long>(slot0 + i + k) * owned,
+                                         h->stream));
                 ++h->launches;
             }
             i += 2;
@@ -228,7 +234,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
         }
         Ctl c = h->ctl;
         c.step = s;
-        c.slot = i;
+        c.slot = slot0 + i;
         c.err = h->d_err;
         c.ghost_lo_end = 0;
         c.ghost_hi_begin = INT_MAX;
@@ -258,7 +264,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt) {
         if (!h->rec_owned.empty()) {
             const int owned = static_cast<int>(h->rec_owned.size());
             SWB_CUDA(launch_samplers(h->u + ((s + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w, owned,
-                                     h->d_traces + static_cast<long long>(i) * owned, h->stream));
+                                     h->d_traces + static_cast<long long>(slot0 + i) * owned, h->stream));
             ++h->launches;
         }
         if (kmask) {
@@ -799,6 +805,78 @@ int swb_apply_adjoint(swb_handle* h, int nt, const float* rec_data, float* src_t
     return SWB_OK;
 }
 
+int swb_apply_snapshots(swb_handle* h, int step0, int nt, int every, float* const* snaps, int n_snaps,
+                        float* step_max_abs, int32_t* first_bad_step, float* rec_traces) {
+    if (!h) return fail(SWB_EINVAL, "null handle");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is already pending");
+    if (step0 < 0 || nt < 0 || every < 1) return fail(SWB_EINVAL, "steps must be non-negative and every >= 1");
+    if (n_snaps != nt / every || (n_snaps > 0 && !snaps))
+        return fail(SWB_EINVAL, "need one snapshot buffer per `every` steps (nt / every of them)");
+    if (h->ctl.wavelet && step0 + nt > h->wavelet_len)
+        return fail(SWB_EINVAL, "source wavelet shorter than the number of steps");
+    SWB_CUDA(cudaSetDevice(h->device));
+    int rc = ensure_smax(h, nt);
+    if (rc) return rc;
+    rc = ensure_traces(h, nt);
+    if (rc) return rc;
+    rc = refresh_ring(h);
+    if (rc) return rc;
+    const size_t own_floats = static_cast<size_t>(h->hi - h->lo) * h->plane;
+    if (n_snaps > 0 && !h->s_d2d) {
+        SWB_CUDA(cudaStreamCreateWithFlags(&h->s_d2d, cudaStreamNonBlocking));
+        SWB_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+        SWB_CUDA(cudaEventCreateWithFlags(&h->ev_step, cudaEventDisableTiming));
+        for (int j = 0; j < swb_handle::kSnapSlots; ++j) {
+            SWB_CUDA(cudaEventCreateWithFlags(&h->ev_d2d[j], cudaEventDisableTiming));
+            SWB_CUDA(cudaEventCreateWithFlags(&h->ev_d2h[j], cudaEventDisableTiming));
+            SWB_CUDA(cudaMalloc(&h->d_stage[j], sizeof(float) * own_floats));
+        }
+    }
+    if (nt > 0) SWB_CUDA(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned) * nt, h->stream));
+    h->launches = 0;
+    h->ctl.smax = h->d_smax;
+    SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+    const size_t row = sizeof(float) * h->n2;
+    int done = 0;
+    for (int i = 0; i < n_snaps; ++i) {
+        // steps of this interval; the first two may run before the previous snapshot's device
+        // copy is complete (the level it copies is overwritten by the third step after it)
+        const int a = std::min(2, every);
+        rc = enqueue_steps(h, step0 + done, a, done);
+        if (rc) return rc;
+        if (i > 0) SWB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_d2d[(i - 1) % swb_handle::kSnapSlots], 0));
+        if (every > a) {
+            rc = enqueue_steps(h, step0 + done + a, every - a, done + a);
+            if (rc) return rc;
+        }
+        done += every;
+        const int lev = (step0 + done) % 3;  // newest level after step step0 + done - 1
+        const int j = i % swb_handle::kSnapSlots;
+        SWB_CUDA(cudaEventRecord(h->ev_step, h->stream));
+        SWB_CUDA(cudaStreamWaitEvent(h->s_d2d, h->ev_step, 0));
+        if (i >= swb_handle::kSnapSlots) SWB_CUDA(cudaStreamWaitEvent(h->s_d2d, h->ev_d2h[j], 0));
+        SWB_CUDA(cudaMemcpyAsync(h->d_stage[j], h->u + lev * h->level_floats + h->gb * h->plane,
+                                 sizeof(float) * own_floats, cudaMemcpyDeviceToDevice, h->s_d2d));
+        SWB_CUDA(cudaEventRecord(h->ev_d2d[j], h->s_d2d));
+        SWB_CUDA(cudaStreamWaitEvent(h->s_d2h, h->ev_d2d[j], 0));
+        SWB_CUDA(cudaMemcpy2DAsync(snaps[i] + static_cast<size_t>(h->lo) * h->n1 * h->n2, row, h->d_stage[j],
+                                   sizeof(float) * h->P2, row, static_cast<size_t>(h->hi - h->lo) * h->n1,
+                                   cudaMemcpyDeviceToHost, h->s_d2h));
+        SWB_CUDA(cudaEventRecord(h->ev_d2h[j], h->s_d2h));
+    }
+    if (n_snaps > 0) SWB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_d2d[(n_snaps - 1) % swb_handle::kSnapSlots], 0));
+    if (nt > done) {
+        rc = enqueue_steps(h, step0 + done, nt - done, done);
+        if (rc) return rc;
+    }
+    SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+    h->pend_step0 = step0;
+    h->pend_nt = nt;
+    h->pending = true;
+    if (h->s_d2h) SWB_CUDA(cudaStreamSynchronize(h->s_d2h));
+    return swb_collect(h, step_max_abs, first_bad_step, rec_traces);
+}
+
 void* swb_stream(swb_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
 // Debug (SWB_TRACE=1): copy the per-CTA timestamps of the last stencil launch.
@@ -835,6 +913,16 @@ int swb_destroy(swb_handle* h) {
                     static_cast<void*>(h->d_adj), static_cast<void*>(h->d_src_trace),
                     static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
+    if (h->s_d2h) cudaStreamSynchronize(h->s_d2h);
+    if (h->s_d2d) cudaStreamSynchronize(h->s_d2d);
+    for (int j = 0; j < swb_handle::kSnapSlots; ++j) {
+        if (h->d_stage[j]) cudaFree(h->d_stage[j]);
+        if (h->ev_d2d[j]) cudaEventDestroy(h->ev_d2d[j]);
+        if (h->ev_d2h[j]) cudaEventDestroy(h->ev_d2h[j]);
+    }
+    if (h->ev_step) cudaEventDestroy(h->ev_step);
+    if (h->s_d2d) cudaStreamDestroy(h->s_d2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);

@@ -412,6 +412,38 @@ class Operator:
         return RunResult(Field(self.problem), smax, wall, 0, (step0 + nt) % 3, traces,
                          st.device_ms * 1e-3)
 
+    def apply_snapshots(self, nt: int, every: int, step0: Optional[int] = None,
+                        out: Optional[list] = None) -> Tuple[RunResult, list]:
+        """apply(nt) plus a snapshot of the newest level after every ``every`` steps, drained
+        to host memory on a copy stream while the following steps run (swb_apply_snapshots).
+        ``out`` may supply the nt // every grid-sized float32 host buffers (pinned for full
+        PCIe bandwidth).  Returns (the RunResult of apply, the snapshot arrays)."""
+        nt, every = int(nt), int(every)
+        step0 = self.step if step0 is None else int(step0)
+        ns = nt // every
+        snaps = out if out is not None else [np.zeros(self.problem.shape, np.float32) for _ in range(ns)]
+        if len(snaps) != ns:
+            raise ValueError(f"need {ns} snapshot buffers")
+        for a in snaps:
+            if a.dtype != np.float32 or a.size != self.problem.cell_count() or not a.flags.c_contiguous:
+                raise ValueError("snapshot buffers must be grid-sized C-contiguous float32")
+        arr = (C.POINTER(C.c_float) * max(ns, 1))(*[N.fptr(a) for a in snaps])
+        smax = np.zeros(nt, np.float32)
+        bad = C.c_int32(-1)
+        n_rec = (0 if self.receivers is None else self.receivers.shape[0]) + \
+            (0 if self.receiver_coords is None else self.receiver_coords.shape[0])
+        traces = np.zeros((nt, n_rec), np.float32) if n_rec else None
+        t0 = time.perf_counter()
+        rc = N.lib.swb_apply_snapshots(self._h, step0, nt, every, arr, ns, N.fptr(smax), C.byref(bad),
+                                       N.fptr(traces) if traces is not None else N.fptr(None))
+        wall = time.perf_counter() - t0
+        if rc != N.SWB_OK:
+            _check(rc, bad.value)
+        self.step = step0 + nt
+        st = self.stats()
+        return (RunResult(Field(self.problem), smax, wall, 0, (step0 + nt) % 3, traces, st.device_ms * 1e-3),
+                snaps)
+
     def apply_adjoint(self, rec_data: np.ndarray) -> np.ndarray:
         """Adjoint of the map source wavelet -> receiver traces (an addition; the reference has
         no adjoint): inject ``rec_data[nt][n_receivers]`` (on-grid receivers

@@ -1,0 +1,47 @@
+"""Wavefield snapshots overlapped with stepping (swb_apply_snapshots): every snapshot equals
+the newest level of a plain stepped run at that step, bit for bit, and the per-step outputs
+equal swb_apply's.  Covers K1, K3 (time_block=2, even and odd intervals) and the plain form."""
+import numpy as np
+import pytest
+
+import paper_1912_00695_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _prob(so=8, nt=24, shape=(36, 40, 70)):
+    rng = np.random.default_rng(4)
+    vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
+    return P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
+                                                   steps=nt, velocity_field=vel, damp_max=0.05, damp_width=4))
+
+
+@pytest.mark.parametrize("form,tb,every", [("factorised", 1, 5), ("factorised", 1, 1), ("factorised", 2, 4),
+                                           ("factorised", 2, 3), ("plain_f64", 1, 6)])
+def test_snapshots_equal_stepped_levels(form, tb, every):
+    nt = 24
+    prob = _prob(nt=nt)
+    rec = np.array([[18, 20, z] for z in range(5, 65, 7)], np.int32)
+    ref = P.Operator(prob, form=form, receivers=rec)
+    want, smax_ref, tr_ref = [], [], []
+    for s in range(nt):
+        r = ref.apply(1, s)
+        smax_ref.append(r.step_max_abs[0])
+        tr_ref.append(r.rec_traces[0])
+        if (s + 1) % every == 0:
+            want.append(ref.get_level((s + 1) % 3))
+    op = P.Operator(prob, form=form, receivers=rec, time_block=tb)
+    res, snaps = op.apply_snapshots(nt, every, 0)
+    assert len(snaps) == nt // every
+    for i, (a, b) in enumerate(zip(snaps, want)):
+        assert np.array_equal(a, b), i
+    assert np.array_equal(res.step_max_abs, np.array(smax_ref, np.float32))
+    assert np.array_equal(res.rec_traces, np.array(tr_ref))
+    assert np.array_equal(op.levels(), ref.levels())
+
+
+def test_snapshots_validate_buffer_count():
+    prob = _prob(nt=10)
+    op = P.Operator(prob)
+    with pytest.raises(ValueError):
+        op.apply_snapshots(10, 3, 0, out=[np.zeros(prob.shape, np.float32)])
