@@ -612,7 +612,15 @@ size_t smem_bytes() {
     X(6, 1, 30, 11, 3, 2)        \
     X(7, 1, 22, 14, 3, 2)        \
     X(8, 1, 22, 11, 3, 4)        \
-    X(8, 1, 22, 14, 3, 4)
+    X(8, 1, 22, 14, 3, 4)        \
+    X(1, 1, 28, 5, 4, 1)         \
+    X(2, 1, 28, 6, 4, 1)         \
+    X(3, 1, 28, 7, 4, 1)         \
+    X(4, 1, 28, 8, 4, 4)         \
+    X(5, 1, 28, 10, 4, 2)        \
+    X(6, 1, 28, 10, 3, 2)        \
+    X(6, 1, 26, 10, 3, 2)        \
+    X(8, 1, 20, 11, 3, 4)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl);
 
@@ -651,9 +659,22 @@ int preferred_su(int H) {
     return 0;  // 0: first matching variant
 }
 
-const Variant* find_variant(int H) {
+int preferred_t1(int H) {
+    const char* env = std::getenv("SWB_T1");
+    if (env && std::atoi(env) > 0) return std::atoi(env);
+    (void)H;
+    return 0;  // 0: first matching variant
+}
+
+// t1_want: tile height chosen by tma_plan (0: any); SWB_T1 overrides it.
+const Variant* find_variant(int H, int t1_want = 0) {
     static const Variant table[] = {SWB_TMA_VARIANTS(SWB_VARIANT_ENTRY)};
     const int r1 = preferred_r1(H), unr = preferred_unr(H), su = preferred_su(H);
+    const int t1 = preferred_t1(H) ? preferred_t1(H) : t1_want;
+    for (const auto& v : table)
+        if (v.H == H && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su) && (t1 == 0 || v.T1 == t1)) return &v;
+    for (const auto& v : table)
+        if (v.H == H && v.R1 == r1 && (unr == 0 || v.UNR == unr) && (t1 == 0 || v.T1 == t1)) return &v;
     for (const auto& v : table)
         if (v.H == H && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su)) return &v;
     for (const auto& v : table)
@@ -716,14 +737,28 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         p.kind = 1;
         p.variant = 2000 + H;
     } else {
-        const Variant* v = find_variant(H);
+        // Tile height: among the K1 heights for this halo, the one whose row tiles waste the
+        // fewest rows of the interior (measured +1-2 % at 256^3 SO 4/8/12 and 512^3 SO 8 over a
+        // fixed height; heights below 28 lose warps and are not auto-selected).
+        int t1_best = 0;
+        double eff_best = -1.0;
+        const int rows = g.y1 - g.y0;
+        for (int cand : {30, 28, 22}) {
+            if ((H <= 6) != (cand >= 28)) continue;
+            const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
+            if (eff > eff_best + 1e-9) {
+                eff_best = eff;
+                t1_best = cand;
+            }
+        }
+        const Variant* v = find_variant(H, t1_best);
         if (!v) return p;
         T1 = v->T1;
         threads = v->threads;
         smem = static_cast<int>(v->smem);
         fn = reinterpret_cast<const void*>(v->fn);
         p.kind = 0;
-        p.variant = 1000 + 100 * (v->R1 - 1) + 10 * v->UNR + H;
+        p.variant = 1000 + 100 * (v->R1 - 1) + 10 * v->UNR + H + 100000 * v->T1;
     }
     p.T1 = T1;
     p.T2 = kT2;
@@ -788,7 +823,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         return p;
     }
     if (p.tb_ok && p.kind == 0) {
-        const Variant* v = find_variant(H);
+        const Variant* v = find_variant(H, p.T1);
         if (cudaFuncSetAttribute(reinterpret_cast<const void*>(v->fn_tb),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
             cudaGetLastError();
@@ -870,7 +905,7 @@ void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp, int n1
 
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s) {
-    const Variant* v = find_variant(plan.H);
+    const Variant* v = find_variant(plan.H, plan.T1);
     if (!plan.ok || (plan.kind == 0 && !v)) return cudaErrorInvalidValue;
     Sched sc;
     sc.nyt = plan.tiles_y;
@@ -893,7 +928,7 @@ cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, cons
 
 cudaError_t launch_tma_tb(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                           const Ctl& c, const TbCtl& tb_in, cudaStream_t s) {
-    const Variant* v = find_variant(plan.H);
+    const Variant* v = find_variant(plan.H, plan.T1);
     if (!plan.ok || !plan.tb_ok || plan.kind != 0 || !v || !tb_in.cnt) return cudaErrorInvalidValue;
     Sched sc;
     sc.nyt = plan.tiles_y;
