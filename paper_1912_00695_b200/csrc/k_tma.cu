@@ -189,6 +189,8 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
             if (it.rows_ok || it.yt + i < g.y1)
                 store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
     } else {
+        // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same
+        // lane masks) and the source plane (the one injected element is patched first)
 #pragma unroll
         for (int i = 0; i < R1; ++i) {
             const int y = it.yt + i;
@@ -200,17 +202,10 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
                                              static_cast<double>(K.dt)));
             }
             const long long idx = xoff + static_cast<long long>(i) * g.P2;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int z = it.zc + e;
-                if (z >= g.z0 && z < g.z1) {
-                    const float v = comp(o, e);
-                    un[idx + e] = v;
-                    if (lo_m) lo_peer[idx + e + static_cast<long long>(pr.lo_shift) * g.plane] = v;
-                    if (hi_m) hi_peer[idx + e + static_cast<long long>(pr.hi_shift) * g.plane] = v;
-                    mine = max(mine, abs_bits(v));
-                }
-            }
+            store_row(un + idx, o, it.zmask, mine);
+            unsigned dummy = 0u;
+            if (lo_m) store_row(lo_peer + idx + static_cast<long long>(pr.lo_shift) * g.plane, o, it.zmask, dummy);
+            if (hi_m) store_row(hi_peer + idx + static_cast<long long>(pr.hi_shift) * g.plane, o, it.zmask, dummy);
         }
     }
     // Temporal blocking, stage 1: publish "this warp has stored one more u[t+1] plane"
@@ -570,7 +565,8 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
         }
     }
     __syncwarp();
-    if (c.sig_lo || c.sig_hi) __threadfence_system();  // peer stores of this thread -> system scope
+    // (peer stores reach system scope through thread 0's __threadfence_system in
+    // signal_neighbours, after the CTA barrier in block_max_commit: fence cumulativity)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
     block_max_commit(mine, c.smax + c.slot);
