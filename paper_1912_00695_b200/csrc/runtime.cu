@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <climits>
@@ -34,6 +37,58 @@ int fail(int code, const std::string& msg) {
     } while (0)
 
 constexpr uint32_t kBlobMagic = 0x53574231u;  // "SWB1"
+
+// Process-wide cache of the large per-handle buffers (u levels, m, damp), keyed by device and
+// exact size: a handle created after another one was destroyed (a new problem of the same
+// grid, the bench's end-to-end run) reuses its HBM instead of paying cudaMalloc/cudaFree
+// (milliseconds each for hundreds of MB).  SWB_NO_POOL=1 disables it.
+struct BufPool {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void*> free_;
+};
+BufPool& pool() {
+    static BufPool* p = new BufPool();  // never destroyed: outlives static handles at exit
+    return *p;
+}
+bool pool_enabled() {
+    static const bool on = std::getenv("SWB_NO_POOL") == nullptr;
+    return on;
+}
+cudaError_t pool_alloc(int device, void** ptr, size_t bytes) {
+    if (pool_enabled()) {
+        std::lock_guard<std::mutex> lk(pool().mu);
+        auto it = pool().free_.find({device, bytes});
+        if (it != pool().free_.end()) {
+            *ptr = it->second;
+            pool().free_.erase(it);
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e == cudaErrorMemoryAllocation && pool_enabled()) {  // give the cache back and retry
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(pool().mu);
+        for (auto it = pool().free_.begin(); it != pool().free_.end();) {
+            if (it->first.first == device) {
+                cudaFree(it->second);
+                it = pool().free_.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        e = cudaMalloc(ptr, bytes);
+    }
+    return e;
+}
+void pool_free(int device, void* ptr, size_t bytes, bool shared = false) {
+    if (!ptr) return;
+    if (!pool_enabled() || shared) {  // IPC-exported memory may still be mapped by a peer
+        cudaFree(ptr);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(pool().mu);
+    pool().free_.insert({{device, bytes}, ptr});
+}
 
 struct IpcBlob {
     uint32_t magic;
@@ -108,6 +163,7 @@ struct swb_handle {
     void* ipc_lo_f = nullptr;
     void* ipc_hi_f = nullptr;
     unsigned long long steps_done = 0;
+    bool exported = false;  // u was exported through CUDA IPC (never recycled through the pool)
     // pending apply
     int pend_step0 = 0, pend_nt = 0;
     bool pending = false;
@@ -390,12 +446,24 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             return cleanup(fail(SWB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
     } while (0)
 
+    const bool prof = std::getenv("SWB_PROFILE_CREATE") != nullptr;  // development timing
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t_last = now();
+    auto mark = [&](const char* what) {
+        if (!prof) return;
+        cudaStreamSynchronize(h->stream);
+        const auto t = now();
+        std::fprintf(stderr, "swb_create %-24s %8.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     SWB_CUDA_C(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    mark("stream");
     SWB_CUDA_C(cudaEventCreate(&h->ev0));
     SWB_CUDA_C(cudaEventCreate(&h->ev1));
-    SWB_CUDA_C(cudaMalloc(&h->u, sizeof(float) * 3 * h->level_floats));
-    SWB_CUDA_C(cudaMalloc(&h->m, sizeof(float) * h->level_floats));
-    SWB_CUDA_C(cudaMalloc(&h->damp, sizeof(float) * h->level_floats));
+    SWB_CUDA_C(pool_alloc(h->device, reinterpret_cast<void**>(&h->u), sizeof(float) * 3 * h->level_floats));
+    SWB_CUDA_C(pool_alloc(h->device, reinterpret_cast<void**>(&h->m), sizeof(float) * h->level_floats));
+    SWB_CUDA_C(pool_alloc(h->device, reinterpret_cast<void**>(&h->damp), sizeof(float) * h->level_floats));
     SWB_CUDA_C(cudaMemsetAsync(h->u, 0, sizeof(float) * 3 * h->level_floats, h->stream));
     SWB_CUDA_C(cudaMemsetAsync(h->m, 0, sizeof(float) * h->level_floats, h->stream));
     SWB_CUDA_C(cudaMemsetAsync(h->damp, 0, sizeof(float) * h->level_floats, h->stream));
@@ -405,6 +473,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     SWB_CUDA_C(cudaMalloc(&h->d_err, sizeof(unsigned)));
     SWB_CUDA_C(cudaMemsetAsync(h->d_err, 0, sizeof(unsigned), h->stream));
 
+    mark("malloc+memset");
     // m / damp for every local plane (ghost planes included; they are never read).
     const size_t row = sizeof(float) * h->n2;
     const float* m_src = p->m + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
@@ -544,6 +613,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_w, rw.data(), sizeof(double) * rw.size(), cudaMemcpyHostToDevice,
                                    h->stream));
     }
+    mark("H2D m/damp, weights, rec");
     // Adjoint output sampler at the source point (owned slab only).
     if (c.has_src) {
         const size_t gi = (static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2];
@@ -557,6 +627,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         SWB_CUDA_C(cudaMemcpyAsync(h->d_src_idx, si.data(), sizeof(long long) * 8, cudaMemcpyHostToDevice, h->stream));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_src_w, sw.data(), sizeof(double) * 8, cudaMemcpyHostToDevice, h->stream));
     }
+    mark("adjoint sampler");
     // Kernel choice: the TMA 2.5D kernel for the factorised form when the plan fits.
     if (h->form == SWB_FORM_FACTORISED) {
         int sms = 148;
@@ -585,6 +656,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     h->stats.launch_steps = (h->time_block >= 2 && h->use_tma && h->plan.tb_ok) ? 2 : 1;
     if (h->stats.launch_steps == 2) h->stats.kernel_variant += 10000;  // K3 (two-step) variant ids
     compute_peer_ranges(h);
+    mark("plan+maps+dflags");
     SWB_CUDA_C(cudaStreamSynchronize(h->stream));
     *out = h;
 #undef SWB_CUDA_C
@@ -902,8 +974,11 @@ int swb_destroy(swb_handle* h) {
     if (h->ipc_hi_u) cudaIpcCloseMemHandle(h->ipc_hi_u);
     if (h->ipc_lo_f) cudaIpcCloseMemHandle(h->ipc_lo_f);
     if (h->ipc_hi_f) cudaIpcCloseMemHandle(h->ipc_hi_f);
-    for (void* q : {static_cast<void*>(h->u), static_cast<void*>(h->m), static_cast<void*>(h->damp),
-                    static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
+    // the big buffers go back to the pool (the stream is idle: synchronised above)
+    pool_free(h->device, h->u, sizeof(float) * 3 * h->level_floats, h->exported);
+    pool_free(h->device, h->m, sizeof(float) * h->level_floats);
+    pool_free(h->device, h->damp, sizeof(float) * h->level_floats);
+    for (void* q : {static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
                     static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
                     static_cast<void*>(h->d_rec_w),
                     static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
@@ -994,6 +1069,7 @@ int swb_export_ghosts(swb_handle* h, void* blob, size_t* blob_len) {
     b.grid = h->plan.grid;
     b.level_floats = h->level_floats;
     SWB_CUDA(cudaIpcGetMemHandle(&b.u_handle, h->u));
+    h->exported = true;
     SWB_CUDA(cudaIpcGetMemHandle(&b.flag_handle, h->d_flags));
     std::memcpy(blob, &b, sizeof b);
     *blob_len = sizeof b;
