@@ -95,16 +95,42 @@ cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ct
 __global__ void k_ring_max(const float* __restrict__ u, long long plane, int P2, int nx0, int nx1,
                            int n1, int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
                            int z_in1, unsigned* out) {
+    // Reads the ring only (about 6 % of a 256^3 level at SO 8), as two flat index spaces with
+    // independent loads: (B) every cell of the rows outside the interior in x or y, (A) the
+    // z ends of the interior rows.
     unsigned mine = 0u;
-    const long long total = static_cast<long long>(nx1 - nx0) * n1 * n2;
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int z = static_cast<int>(t % n2);
-        const int y = static_cast<int>((t / n2) % n1);
-        const int x = nx0 + static_cast<int>(t / (static_cast<long long>(n2) * n1));
-        const bool interior = x >= x_in0 && x < x_in1 && y >= y_in0 && y < y_in1 && z >= z_in0 &&
-                              z < z_in1;
-        if (!interior) mine = max(mine, abs_bits(u[x * plane + y * P2 + z]));
+    const int xi0 = max(x_in0, nx0), xi1 = max(min(x_in1, nx1), xi0);
+    const int nxl = xi0 - nx0, nxo = nxl + (nx1 - xi1), nxi = xi1 - xi0;
+    const int yi0 = min(y_in0, n1), yi1 = max(min(y_in1, n1), yi0);
+    const int nyl = yi0, nyo = nyl + (n1 - yi1), nyi = yi1 - yi0;
+    const int zlo = min(z_in0, n2), zhi = max(min(z_in1, n2), zlo), edge = zlo + (n2 - zhi);
+    const long long rowsB = static_cast<long long>(nxo) * n1 + static_cast<long long>(nxi) * nyo;
+    const long long totB = rowsB * n2, totA = static_cast<long long>(nxi) * nyi * edge;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < totB + totA; t += stride) {
+        int x, y, z;
+        if (t < totB) {
+            const long long r = t / n2;
+            z = static_cast<int>(t % n2);
+            if (r < static_cast<long long>(nxo) * n1) {
+                const int i = static_cast<int>(r / n1);
+                x = i < nxl ? nx0 + i : xi1 + (i - nxl);
+                y = static_cast<int>(r % n1);
+            } else {
+                const long long r2 = r - static_cast<long long>(nxo) * n1;
+                const int j = static_cast<int>(r2 % nyo);
+                x = xi0 + static_cast<int>(r2 / nyo);
+                y = j < nyl ? j : yi1 + (j - nyl);
+            }
+        } else {
+            const long long t2 = t - totB;
+            const long long r = t2 / edge;
+            const int e = static_cast<int>(t2 % edge);
+            x = xi0 + static_cast<int>(r / nyi);
+            y = yi0 + static_cast<int>(r % nyi);
+            z = e < zlo ? e : zhi + (e - zlo);
+        }
+        mine = max(mine, abs_bits(u[x * plane + static_cast<long long>(y) * P2 + z]));
     }
     block_max_commit(mine, out);
 }
@@ -214,8 +240,8 @@ cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, in
                             int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
                             int z_in1, unsigned* out, cudaStream_t s) {
     if (nx1 <= nx0) return cudaSuccess;
-    k_ring_max<<<592, 256, 0, s>>>(u, plane, P2, nx0, nx1, n1, n2, x_in0, x_in1, y_in0, y_in1,
-                                   z_in0, z_in1, out);
+    k_ring_max<<<148 * 8, 256, 0, s>>>(u, plane, P2, nx0, nx1, n1, n2, x_in0, x_in1, y_in0, y_in1,
+                                       z_in0, z_in1, out);
     return cudaGetLastError();
 }
 
