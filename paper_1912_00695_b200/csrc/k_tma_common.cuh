@@ -43,13 +43,18 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until the phase
+// completes (or the hint expires) instead of waking to re-poll and taking issue slots.
+#ifndef SWB_MBAR_SUSPEND_NS
+#define SWB_MBAR_SUSPEND_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(SWB_MBAR_SUSPEND_NS)
         : "memory");
 }
 __device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int c0, int c1,
