@@ -152,6 +152,10 @@ __global__ void k_receivers(const float* __restrict__ un, const long long* __res
 // slab have index -1 (their partial sums are added across slabs by the caller).
 __global__ void k_samplers(const float* __restrict__ un, const long long* __restrict__ idx,
                            const double* __restrict__ w, int n, float* __restrict__ out) {
+    // Launched with programmatic stream serialization: wait for the stencil step (the previous
+    // grid) to complete, and let the next step's stencil kernel start its prologue right away.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < n) {
         double v = 0.0;
@@ -197,8 +201,16 @@ cudaError_t launch_inject(float* un, const long long* idx, const double* w, int 
 cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
                             cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    k_samplers<<<ceil_div(n, 128), 128, 0, s>>>(un, idx, w, n, out);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ceil_div(n, 128));
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_samplers, un, idx, w, n, out);
 }
 
 // Halo-exchange ordering: spin until every linked neighbour has completed at least
