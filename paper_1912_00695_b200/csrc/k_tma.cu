@@ -619,6 +619,7 @@ size_t smem_bytes() {
     X(5, 1, 28, 10, 4, 2)        \
     X(6, 1, 28, 10, 3, 2)        \
     X(6, 1, 26, 10, 3, 2)        \
+    X(6, 1, 28, 10, 3, 4)        \
     X(8, 1, 20, 11, 3, 4)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl);
@@ -647,8 +648,9 @@ int preferred_r1(int H) {
 int preferred_unr(int H) {
     const char* env = std::getenv("SWB_UNR");
     if (env && env[0] >= '1' && env[0] <= '9') return env[0] - '0';
-    // measured on B200 at 256^3 and 512^3: 4 for SO 8 and 16, 2 for SO 10-14
-    return H == 4 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
+    // measured on B200 at 256^3 and 512^3: 4 for SO 8, 12 and 16, 2 for SO 10/14
+    // (SO 8 runs the rotating queue, which ignores UNR)
+    return H == 4 || H == 6 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
 }
 
 int preferred_su(int H) {
