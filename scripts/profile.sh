@@ -5,8 +5,10 @@
 #  3. one --set full capture of K3 (k_tma<...,1>, two steps per launch) at SO 4 / 8 / 16
 set -x
 mkdir -p gpurun_out
+# the driver's default bench command; ncu records the first 400 kernel launches (setup, the
+# 10 warm-up steps and 380+ timed steps), the rest of the run executes unprofiled
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > gpurun_out/launches_bench.log 2>&1
+    python bench.py > gpurun_out/launches_bench.log 2>&1
 for so in ${SOS:-4 8 12 16}; do
   ncu --set full --clock-control none --import-source on -k regex:k_tma -s 6 -c 1 \
       -o gpurun_out/tma_so$so python scripts/probe_perf.py factorised $so 256 8 > gpurun_out/ncu_so$so.log 2>&1
