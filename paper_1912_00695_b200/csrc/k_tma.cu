@@ -54,7 +54,86 @@ struct Pub {
     unsigned long long base;  // epoch tag
     unsigned* done;           // smem [16] per-plane warp tallies, [16] = (seq << 16) | planes complete
     unsigned seq;             // this CTA's item sequence number (tags `complete`)
+    int H;                    // halo (output plane n of an item arrives at step n + 2H)
+    int ncw;                  // consumer warps of the CTA
 };
+
+// Fused epilogue of one output plane: 128-bit stores (plus peer stores into the neighbours'
+// ghost planes, and the source injection with the reference's two roundings), the max|u|
+// fold, and the K3 stage-1 progress publication.
+template <int R1>
+__device__ __forceinline__ void epilogue_store(const float4* out, const float4* mv, int p, const Item& it,
+                                               unsigned& mine, float* un, float* lo_peer, float* hi_peer,
+                                               const Geo& g, const Coef& K, const Ctl& c, const Peer& pr,
+                                               const Pub& pub, int j) {
+    const long long xoff = static_cast<long long>(p) * g.plane + it.gcol;
+    const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
+    const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
+    const bool src_plane = c.has_src && p == c.src_x;
+    if (!(lo_m || hi_m || src_plane)) {
+        // common path: plain stores (rows past the interior are skipped warp-uniformly)
+#pragma unroll
+        for (int i = 0; i < R1; ++i)
+            if (it.rows_ok || it.yt + i < g.y1)
+                store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+    } else {
+        // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same
+        // lane masks) and the source plane (the one injected element is patched first)
+#pragma unroll
+        for (int i = 0; i < R1; ++i) {
+            const int y = it.yt + i;
+            float4 o = out[i];
+            if (y >= g.y1) continue;
+            if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
+                const int e = c.src_z - it.zc;
+                set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
+                                             static_cast<double>(K.dt)));
+            }
+            const long long idx = xoff + static_cast<long long>(i) * g.P2;
+            store_row(un + idx, o, it.zmask, mine);
+            unsigned dummy = 0u;
+            if (lo_m) store_row(lo_peer + idx + static_cast<long long>(pr.lo_shift) * g.plane, o, it.zmask, dummy);
+            if (hi_m) store_row(hi_peer + idx + static_cast<long long>(pr.hi_shift) * g.plane, o, it.zmask, dummy);
+        }
+    }
+    // Temporal blocking, stage 1: publish "this warp has stored one more u[t+1] plane"
+    // (the stage-2 CTAs wait on these counters before reading the plane through TMA).
+    if (pub.cnt) {
+        // A plane is done when its last warp tallies it; that warp records it in `complete`
+        // (CTA scope).  The gpu-scope release (fence + red.max) is paid by the FIRST warp to
+        // finish a later plane -- a warp that is ahead of the others, so the fence does not
+        // stall the slowest warp (which gates the whole CTA through the rings).  The item's
+        // final plane is published by its last warp.
+        __syncwarp();  // orders the warp's stores before lane 0's tally (bar.warp.sync)
+        if ((threadIdx.x & 31) == 0) {
+            const int n = j - 2 * pub.H;  // output plane index within the item
+            unsigned old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old) : "r"(smem_addr(pub.done + (n & 15))) : "memory");
+            const unsigned tag = pub.seq << 16;
+            if (old == static_cast<unsigned>(pub.ncw - 1)) {  // last warp for plane n
+                pub.done[n & 15] = 0u;
+                asm volatile("red.release.cta.shared::cta.max.u32 [%0], %1;"
+                             :: "r"(smem_addr(pub.done + 16)), "r"(tag | static_cast<unsigned>(n + 1)) : "memory");
+                if (n + 1 == it.xb - it.xa) {  // the item's final plane
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
+                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(n + 1)) : "memory");
+                }
+            } else if (old == 0u && n > 0) {  // first warp for plane n: publish what is complete
+                unsigned done_;
+                asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                             : "=r"(done_) : "r"(smem_addr(pub.done + 16)) : "memory");
+                if ((done_ & ~0xffffu) == tag && (done_ & 0xffffu) != 0u) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
+                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(done_ & 0xffffu))
+                                 : "memory");
+                }
+            }
+        }
+    }
+}
 
 template <int H, int R1, int T1, int SU, int SA, int QN, int U>
 __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const Item& it,
@@ -177,74 +256,212 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
         }
         out[i] = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    // ---- fused epilogue ----
-    const long long xoff = static_cast<long long>(p) * g.plane + it.gcol;
-    const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
-    const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
-    const bool src_plane = c.has_src && p == c.src_x;
-    if (!(lo_m || hi_m || src_plane)) {
-        // common path: plain stores (rows past the interior are skipped warp-uniformly)
-#pragma unroll
-        for (int i = 0; i < R1; ++i)
-            if (it.rows_ok || it.yt + i < g.y1)
-                store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+    epilogue_store<R1>(out, mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+}
+
+// ---- K1 with the dim-0 queue in tensor memory (UNR == 0 variants) -----------------------
+// Each consumer thread owns one TMEM lane (its warp's lane quadrant) and a 128-column block
+// (4 warps share a quadrant): a ring of 32 float4 slots holding u[t] of its 4 points for the
+// last 32 planes.  The x-stencil reads its 2H neighbours with tcgen05.ld instead of keeping
+// 2H+UNR float4 in registers, so the register queue (and its shift moves) disappears and the
+// plane loop needs no unrolling.  TMEM is an extra on-chip store with its own datapath: the
+// loads do not use the shared-memory pipe that the y/z stencil saturates.
+__device__ __forceinline__ void tm_st4(unsigned addr, const float4& v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ float4 tm_ld4(unsigned addr) {
+    float4 v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+// tcgen05.wait::ld, with the loaded values routed through the asm so that no use of them can
+// be scheduled before the wait (the loads' outputs are otherwise "ready" at issue).
+template <int N>
+__device__ __forceinline__ void tm_wait_ld(float4 (&v)[N]) {
+    static_assert(N <= 7, "at most 28 asm operands per wait");
+    if constexpr (N == 0) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    } else if constexpr (N == 1) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(v[0].x), "+f"(v[0].y), "+f"(v[0].z), "+f"(v[0].w) :: "memory");
     } else {
-        // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same
-        // lane masks) and the source plane (the one injected element is patched first)
+        asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(v[0].x), "+f"(v[0].y), "+f"(v[0].z), "+f"(v[0].w),
+                     "+f"(v[1].x), "+f"(v[1].y), "+f"(v[1].z), "+f"(v[1].w) :: "memory");
 #pragma unroll
-        for (int i = 0; i < R1; ++i) {
-            const int y = it.yt + i;
-            float4 o = out[i];
-            if (y >= g.y1) continue;
-            if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
-                const int e = c.src_z - it.zc;
-                set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
-                                             static_cast<double>(K.dt)));
+        for (int i = 2; i < N; ++i)
+            asm volatile("" : "+f"(v[i].x), "+f"(v[i].y), "+f"(v[i].z), "+f"(v[i].w) :: "memory");
+    }
+}
+
+template <int H, int R1, int T1, int SU, int SA>
+__device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item& it, const float* ucol,
+                                                 const float* acol, const unsigned* aflag, unsigned full_u,
+                                                 unsigned empty_u, unsigned full_a, unsigned empty_a, unsigned& su,
+                                                 unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
+                                                 unsigned& mine, float* un, float* lo_peer, float* hi_peer,
+                                                 const Geo& g, const Coef& K, const Ctl& c, const Peer& pr,
+                                                 const Pub& pub) {
+    static_assert(R1 == 1 && H >= 2 && 2 * H + 1 <= 32, "TMEM queue: one row per thread, ring of 32 planes");
+    using C = Cfg<H, R1, T1>;
+    const int q = it.q0 + it.dir * j;
+    mbar_wait(full_u + 8 * su, pu);
+    const float* plane_q = ucol + su * (C::UPLANE / 4);
+    const float4 cq = *reinterpret_cast<const float4*>(plane_q);
+    tm_st4(tq + 4u * static_cast<unsigned>(j & 31), cq);
+    if (!(q >= it.xa && q < it.xb)) mbar_arrive(empty_u + 8 * su);
+    ring_next<SU>(su, pu);
+    if (j < 2 * H) return;
+    const int p = q - it.dir * H;
+    const int jc = j - H;  // step index of plane p
+    const float* rowc = ucol + sp * (C::UPLANE / 4);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // earlier planes' stores landed
+    float w[4 + 2 * C::A];
+#pragma unroll
+    for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
+        const float4 v = *reinterpret_cast<const float4*>(rowc - C::A + 4 * jj);
+        w[4 * jj] = v.x;
+        w[4 * jj + 1] = v.y;
+        w[4 * jj + 2] = v.z;
+        w[4 * jj + 3] = v.w;
+    }
+    float2 al = splat(0.f), ah = splat(0.f);
+    // far half of the x-neighbours: k = H .. KB+1 (plane p+H is the one that just arrived)
+    constexpr int KB = H / 2;
+    {
+        float4 xv[2 * (H - KB) - 1];
+#pragma unroll
+        for (int k = H; k > KB; --k) {
+            xv[H - k] = tm_ld4(tq + 4u * static_cast<unsigned>((jc - k) & 31));
+            if (k != H) xv[2 * (H - KB) - 1 - (H - k)] = tm_ld4(tq + 4u * static_cast<unsigned>((jc + k) & 31));
+        }
+        tm_wait_ld(xv);
+#pragma unroll
+        for (int k = H; k > KB; --k) {
+            const float2 ck = splat(K.c[k]);
+            const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2);
+            const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2);
+            const float4 xm = xv[H - k];
+            const float4 xp = k == H ? cq : xv[2 * (H - KB) - 1 - (H - k)];
+            float2 zl, zh;
+            if ((k & 1) == 0) {
+                zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]), make_float2(w[C::A + k], w[C::A + 1 + k]));
+                zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
+                          make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
+            } else {
+                zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
+                zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k], w[C::A + 3 - k] + w[C::A + 3 + k]);
             }
-            const long long idx = xoff + static_cast<long long>(i) * g.P2;
-            store_row(un + idx, o, it.zmask, mine);
-            unsigned dummy = 0u;
-            if (lo_m) store_row(lo_peer + idx + static_cast<long long>(pr.lo_shift) * g.plane, o, it.zmask, dummy);
-            if (hi_m) store_row(hi_peer + idx + static_cast<long long>(pr.hi_shift) * g.plane, o, it.zmask, dummy);
+            const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
+            const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
+            al = fma2(ck, sl, al);
+            ah = fma2(ck, sh, ah);
         }
     }
-    // Temporal blocking, stage 1: publish "this warp has stored one more u[t+1] plane"
-    // (the stage-2 CTAs wait on these counters before reading the plane through TMA).
-    if (pub.cnt) {
-        // A plane is done when its last warp tallies it; that warp records it in `complete`
-        // (CTA scope).  The gpu-scope release (fence + red.max) is paid by the FIRST warp to
-        // finish a later plane -- a warp that is ahead of the others, so the fence does not
-        // stall the slowest warp (which gates the whole CTA through the rings).  The item's
-        // final plane is published by its last warp.
-        __syncwarp();  // orders the warp's stores before lane 0's tally (bar.warp.sync)
-        if ((threadIdx.x & 31) == 0) {
-            const int n = j - 2 * H;  // output plane index within the item
-            unsigned old;
-            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                         : "=r"(old) : "r"(smem_addr(pub.done + (n & 15))) : "memory");
-            const unsigned tag = pub.seq << 16;
-            if (old == C::NCW - 1) {  // last warp for plane n
-                pub.done[n & 15] = 0u;
-                asm volatile("red.release.cta.shared::cta.max.u32 [%0], %1;"
-                             :: "r"(smem_addr(pub.done + 16)), "r"(tag | static_cast<unsigned>(n + 1)) : "memory");
-                if (n + 1 == it.xb - it.xa) {  // the item's final plane
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
-                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(n + 1)) : "memory");
-                }
-            } else if (old == 0u && n > 0) {  // first warp for plane n: publish what is complete
-                unsigned done_;
-                asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
-                             : "=r"(done_) : "r"(smem_addr(pub.done + 16)) : "memory");
-                if ((done_ & ~0xffffu) == tag && (done_ & 0xffffu) != 0u) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;"
-                                 :: "l"(pub.cnt), "l"(pub.base + static_cast<unsigned long long>(done_ & 0xffffu))
-                                 : "memory");
-                }
-            }
+    float4 u0;
+    float4 xm1, xp1;
+    {
+        // near half: k = KB .. 2, then the k = 1 ring and the centre
+        float4 xv[2 * KB + 1];
+#pragma unroll
+        for (int k = KB; k >= 1; --k) {
+            xv[KB - k] = tm_ld4(tq + 4u * static_cast<unsigned>((jc - k) & 31));
+            xv[2 * KB - (KB - k)] = tm_ld4(tq + 4u * static_cast<unsigned>((jc + k) & 31));
         }
+        xv[KB] = tm_ld4(tq + 4u * static_cast<unsigned>(jc & 31));
+        if constexpr (2 * KB + 1 <= 7) {
+            tm_wait_ld(xv);
+        } else {
+            float4 (&a)[7] = *reinterpret_cast<float4 (*)[7]>(&xv[0]);
+            tm_wait_ld(a);
+#pragma unroll
+            for (int i = 7; i < 2 * KB + 1; ++i)
+                asm volatile("" : "+f"(xv[i].x), "+f"(xv[i].y), "+f"(xv[i].z), "+f"(xv[i].w) :: "memory");
+        }
+#pragma unroll
+        for (int k = KB; k >= 2; --k) {
+            const float2 ck = splat(K.c[k]);
+            const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2);
+            const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2);
+            const float4 xm = xv[KB - k];
+            const float4 xp = xv[2 * KB - (KB - k)];
+            float2 zl, zh;
+            if ((k & 1) == 0) {
+                zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]), make_float2(w[C::A + k], w[C::A + 1 + k]));
+                zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
+                          make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
+            } else {
+                zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
+                zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k], w[C::A + 3 - k] + w[C::A + 3 + k]);
+            }
+            const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
+            const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
+            al = fma2(ck, sl, al);
+            ah = fma2(ck, sh, ah);
+        }
+        u0 = xv[KB];
+        xm1 = xv[KB - 1];
+        xp1 = xv[KB + 1];
     }
+    float2 acc[2];
+    {
+        // k = 1 ring in difference form, all three axes
+        const float4 ym = *reinterpret_cast<const float4*>(rowc - C::W2);
+        const float4 yp = *reinterpret_cast<const float4*>(rowc + C::W2);
+        const float4& xm = xm1;
+        const float4& xp = xp1;
+        const float2 ul = lo2(u0), uh = hi2(u0);
+        float dz[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float ue = comp(u0, e);
+            dz[e] = (w[C::A + e - 1] - ue) + (w[C::A + e + 1] - ue);
+        }
+        float2 dl = add2(sub2(lo2(xm), ul), sub2(lo2(xp), ul));
+        dl = add2(dl, add2(sub2(lo2(ym), ul), sub2(lo2(yp), ul)));
+        dl = add2(dl, make_float2(dz[0], dz[1]));
+        float2 dh = add2(sub2(hi2(xm), uh), sub2(hi2(xp), uh));
+        dh = add2(dh, add2(sub2(hi2(ym), uh), sub2(hi2(yp), uh)));
+        dh = add2(dh, make_float2(dz[2], dz[3]));
+        const float2 c1 = splat(K.c[1]);
+        acc[0] = fma2(c1, dl, al);
+        acc[1] = fma2(c1, dh, ah);
+    }
+    // ---- aux tiles: u[t-1], m, damp ----
+    mbar_wait(full_a + 8 * sa, pa_);
+    const float* aux = acol + sa * (3 * C::ATILE / 4);
+    const bool has_damp = aflag[sa] != 0u;
+    const float4 upv = *reinterpret_cast<const float4*>(aux);
+    const float4 mv = *reinterpret_cast<const float4*>(aux + C::ATILE / 4);
+    const float4 dv = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    mbar_arrive(empty_a + 8 * sa);
+    mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
+    ring_next<SA>(sa, pa_);
+    if (++sp == SU) sp = 0;
+    // ---- combine ----
+    const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+    const float2 hdt = splat(K.half_dt);
+    float4 out;
+    {
+        float2 res[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 ucv = h ? hi2(u0) : lo2(u0);
+            const float2 um = h ? hi2(upv) : lo2(upv);
+            const float2 m = h ? hi2(mv) : lo2(mv);
+            const float2 dm = h ? hi2(dv) : lo2(dv);
+            const float2 Lr = fma2(R3, ucv, acc[h]);
+            const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
+            const float2 gg = mul2(dm, hdt);
+            const float2 num = fma2(sub2(m, gg), sub2(ucv, um), Lk);
+            res[h] = add2(ucv, div2(num, add2(m, gg)));
+        }
+        out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
+    }
+    epilogue_store<R1>(&out, &mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
 }
 
 template <int H, int R1, int T1, int SU, int SA, int U>
@@ -319,7 +536,8 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     constexpr int NQ = C::NQ;
     // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
     // renaming; large halos: shift the queue (keeps the loop body small for the I-cache).
-    constexpr bool kUnroll = H <= SWB_UNROLL_MAXH;
+    constexpr bool kTQ = UNR == 0;  // dim-0 queue in tensor memory
+    constexpr bool kUnroll = !kTQ && H <= SWB_UNROLL_MAXH;
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* uring = smem;
     unsigned char* aring = smem + SU * C::UPLANE;
@@ -344,7 +562,18 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    __shared__ unsigned tmem_base;
+    if constexpr (kTQ) {
+        // all 512 TMEM columns: 4 warps per lane quadrant x 128 columns (32 float4 slots) each
+        if ((threadIdx.x >> 5) == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                smem_addr(&tmem_base)) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if constexpr (kTQ) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // Programmatic dependent launch: everything above overlapped the previous step's tail;
     // u[t], u[t-1] written by that step are only touched after this point.
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -508,7 +737,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
         const float* ucol = reinterpret_cast<const float*>(uring) + (r0 + H) * C::W2 + C::A + 4 * tz;
         const float* acol = reinterpret_cast<const float*>(aring) + r0 * kT2 + 4 * tz;
         float4 Q[R1][kUnroll ? NQ : 1];   // rotating register queue (H <= 3)
-        float4 Qs[R1][kUnroll ? 1 : 2 * H + UNR];  // shifting register queue (H >= 4)
+        float4 Qs[R1][(kUnroll || kTQ) ? 1 : 2 * H + UNR];  // shifting register queue
         unsigned su = 0, pu = 0, sp = 0, sa = 0, pa_ = 0;
         for (int item = first; item < nitems; item += G) {
             Pub pub;
@@ -516,6 +745,8 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             pub.base = epoch;
             pub.done = tally;
             pub.seq = static_cast<unsigned>((item - first) / G + 1);
+            pub.H = H;
+            pub.ncw = C::NCW;
             const int col = item % sc.ncol, chunk = item / sc.ncol;
             Item it;
             it.xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
@@ -541,7 +772,15 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                 mbar_wait(full_u + 8 * s2, p2);
                 c.trace[4 * blockIdx.x + 1] = gtimer();
             }
-            if constexpr (kUnroll) {
+            if constexpr (kTQ) {
+                const unsigned tq = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                                    128u * static_cast<unsigned>(warp >> 2);
+#pragma unroll 1
+                for (int j = 0; j < it.nq; ++j)
+                    consumer_step_tq<H, R1, T1, SU, SA>(tq, j, it, ucol, acol, aflag, full_u, empty_u, full_a,
+                                                        empty_a, su, pu, sp, sa, pa_, mine, un, lo_peer, hi_peer,
+                                                        g, K, c, pr, pub);
+            } else if constexpr (kUnroll) {
 #pragma unroll 1
                 for (int jb = 0; jb < it.nq; jb += NQ)
                     Unrolled<H, R1, T1, SU, SA, 0>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
@@ -569,7 +808,14 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     // signal_neighbours, after the CTA barrier in block_max_commit: fence cumulativity)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
-    block_max_commit(mine, c.smax + c.slot);
+    if constexpr (kTQ) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    block_max_commit(mine, c.smax + c.slot);  // (contains the CTA barrier)
+    if constexpr (kTQ) {
+        if ((threadIdx.x >> 5) == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        }
+    }
     signal_neighbours(c);
     if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
 }
@@ -620,6 +866,8 @@ size_t smem_bytes() {
     X(6, 1, 28, 10, 3, 2)        \
     X(6, 1, 26, 10, 3, 2)        \
     X(6, 1, 28, 10, 3, 4)        \
+    X(8, 1, 30, 10, 2, 0)        \
+    X(6, 1, 30, 10, 3, 0)        \
     X(8, 1, 20, 11, 3, 4)
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl);
@@ -647,7 +895,7 @@ int preferred_r1(int H) {
 
 int preferred_unr(int H) {
     const char* env = std::getenv("SWB_UNR");
-    if (env && env[0] >= '1' && env[0] <= '9') return env[0] - '0';
+    if (env && env[0] >= '0' && env[0] <= '9') return env[0] - '0';  // 0: TMEM queue variants
     // measured on B200 at 256^3 and 512^3: 4 for SO 8, 12 and 16, 2 for SO 10/14
     // (SO 8 runs the rotating queue, which ignores UNR)
     return H == 4 || H == 6 || H == 8 ? 4 : (H >= 5 ? 2 : 1);

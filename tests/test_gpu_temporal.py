@@ -92,3 +92,18 @@ def test_k3_rejects_deeper_blocking():
     prob = _problem((20, 20, 20), 4, 4)
     with pytest.raises(ValueError):
         P.Operator(prob, time_block=3)
+
+
+@pytest.mark.parametrize("so", [12, 16])
+def test_tmem_queue_variant_bitwise_equals_k1(so, monkeypatch):
+    """The K1 variant with the dim-0 queue in tensor memory (SWB_UNR=0; slower, kept
+    as an option) runs the same arithmetic, so it must agree with the register queue bit for bit."""
+    shape, nt = (52, 54, 70), 9
+    prob = _problem(shape, so, nt, seed=so)
+    l1, m1, _, s1 = _run(prob, nt, 1)
+    monkeypatch.setenv("SWB_UNR", "0")
+    monkeypatch.setenv("SWB_T1", "30")
+    lt, mt, _, st = _run(prob, nt, 1)
+    assert st.kernel_variant % 100 == so // 2 and (st.kernel_variant // 10) % 10 == 0
+    assert np.array_equal(l1, lt)
+    assert np.array_equal(m1, mt)
