@@ -63,3 +63,18 @@ def test_smallest_grids(so):
     fast = P.run(prob, dse=P.DseLevel.aggressive)
     fl = fast.final_level
     assert rel_l2(fast.u.data[fl], ref["levels"][fl]) <= 1e-5
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_smem_queue_kernel_variant(so, monkeypatch):
+    """The shared-memory-queue TMA kernel (k_sq.cu, SWB_KERNEL=sq; slower than the register
+    queue, kept for comparison) is a valid factorised kernel: <= 1e-5 against the oracle."""
+    monkeypatch.setenv("SWB_KERNEL", "sq")
+    shape, nt = (44, 46, 70), 30
+    prob, ocfg = _pair(shape, so, nt, seed=so)
+    ref = O.port_run(ocfg)
+    op = P.Operator(prob)
+    assert op.stats().kernel_variant == 2000 + so // 2
+    op.apply(nt, 0)
+    fl = nt % 3
+    assert rel_l2(op.get_level(fl), ref["levels"][fl]) <= 1e-5
