@@ -7,11 +7,12 @@ behind the C-ABI in include/swb.h.  See DESIGN.md.
 from .wave import (DseLevel, Field, InstabilityError, Operator, RunOptions, RunResult,
                    SourceSpec, WaveProblem, WaveProblemConfig, cfl_dt, fd_coefficients,
                    form_for, make_wave_problem, parse_dse_level, ricker_amplitude,
-                   ricker_wavelet, rounded_weights, run, write_snapshot)
+                   ricker_wavelet, rounded_weights, run, write_snapshot, read_snapshot,
+                   write_checkpoint)
 
 __all__ = [
     "DseLevel", "Field", "InstabilityError", "Operator", "RunOptions", "RunResult",
     "SourceSpec", "WaveProblem", "WaveProblemConfig", "cfl_dt", "fd_coefficients", "form_for",
     "make_wave_problem", "parse_dse_level", "ricker_amplitude", "ricker_wavelet",
-    "rounded_weights", "run", "write_snapshot",
+    "rounded_weights", "run", "write_snapshot", "read_snapshot", "write_checkpoint",
 ]

@@ -412,6 +412,17 @@ class Operator:
         return RunResult(Field(self.problem), smax, wall, 0, (step0 + nt) % 3, traces,
                          st.device_ms * 1e-3)
 
+    def restore(self, directory: str, stem: str, step: int) -> None:
+        """Resume from write_checkpoint(directory, stem, op) taken at ``step``: loads u[step]
+        and u[step-1] into the levels the next step reads; apply() continues at ``step``."""
+        cur, mc = read_snapshot(os.path.join(directory, f"{stem}_{step:06d}"))
+        prev, mp = read_snapshot(os.path.join(directory, f"{stem}_{step - 1:06d}"))
+        if mc["shape"] != tuple(self.problem.shape) or mp["step"] != step - 1 or mc["step"] != step:
+            raise ValueError("checkpoint does not match this problem/step")
+        self.set_level(step % 3, cur)
+        self.set_level((step + 2) % 3, prev)
+        self.step = step
+
     def apply_snapshots(self, nt: int, every: int, step0: Optional[int] = None,
                         out: Optional[list] = None) -> Tuple[RunResult, list]:
         """apply(nt) plus a snapshot of the newest level after every ``every`` steps, drained
@@ -570,6 +581,37 @@ def write_snapshot(directory: str, stem: str, step: int, field: Field, level: in
         f.write("spacing=" + ",".join(_fmt_double(h) for h in problem.spacing) + "\n")
         f.write(f"step={step}\n")
     return base
+
+
+def read_snapshot(base: str) -> Tuple[np.ndarray, dict]:
+    """Inverse of write_snapshot: the grid-sized FP32 level stored at ``<base>.f32`` and the
+    sidecar's ``shape``/``spacing``/``step`` (an addition: the reference only writes snapshots)."""
+    meta = {}
+    with open(base + ".meta") as f:
+        for line in f:
+            if "=" in line:
+                k, v = line.strip().split("=", 1)
+                meta[k] = v
+    shape = tuple(int(x) for x in meta["shape"].split(","))
+    meta = {"shape": shape, "spacing": tuple(float(x) for x in meta["spacing"].split(",")),
+            "step": int(meta["step"])}
+    data = np.fromfile(base + ".f32", dtype="<f4")
+    if data.size != int(np.prod(shape)):
+        raise ValueError(f"{base}.f32 holds {data.size} values, the sidecar says {shape}")
+    return data.reshape(shape).astype(np.float32), meta
+
+
+def write_checkpoint(directory: str, stem: str, op: "Operator") -> Tuple[str, str]:
+    """Restart point of an Operator at its current step s, as two reference-format snapshots:
+    u[s] (``<stem>_<s>``) and u[s-1] (``<stem>_<s-1>``) -- the two levels the next step reads
+    (RunOptions::initial_u semantics, src/executor.cpp:387-393)."""
+    s = op.step
+    if s < 1:
+        raise ValueError("a checkpoint needs at least one completed step")
+    f = Field(op.problem, op.levels())
+    a = write_snapshot(directory, stem, s, f, s % 3, op.problem)
+    b = write_snapshot(directory, stem, s - 1, f, (s + 2) % 3, op.problem)
+    return a, b
 
 
 def _fmt_double(v: float) -> str:

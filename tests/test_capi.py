@@ -114,3 +114,13 @@ def test_write_snapshot_format(tmp_path):
     data = np.fromfile(base + ".f32", "<f4")
     assert np.array_equal(data, np.arange(120, 240, dtype=np.float32))
     assert open(base + ".meta").read() == "shape=4,5,6\nspacing=10,12.5,7\nstep=7\n"
+
+
+def test_snapshot_round_trip(tmp_path):
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=(5, 6, 7), spacing=(10.0, 12.5, 15.0), space_order=2, steps=3))
+    rng = np.random.default_rng(0)
+    lev = rng.standard_normal((3, 5, 6, 7)).astype(np.float32)
+    base = P.write_snapshot(str(tmp_path), "u", 12, P.Field(prob, lev), 2, prob)
+    data, meta = P.read_snapshot(base)
+    assert np.array_equal(data, lev[2])
+    assert meta == {"shape": (5, 6, 7), "spacing": (10.0, 12.5, 15.0), "step": 12}

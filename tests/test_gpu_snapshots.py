@@ -45,3 +45,23 @@ def test_snapshots_validate_buffer_count():
     op = P.Operator(prob)
     with pytest.raises(ValueError):
         op.apply_snapshots(10, 3, 0, out=[np.zeros(prob.shape, np.float32)])
+
+
+@pytest.mark.parametrize("form", ["factorised", "plain_f64"])
+def test_checkpoint_restart_bitwise(form, tmp_path):
+    """write_checkpoint + Operator.restore (reference snapshot format, two levels) resumes a run
+    exactly: 11 + 13 steps through a checkpoint == 24 steps straight."""
+    prob = _prob(nt=24)
+    rec = np.array([[18, 20, z] for z in range(5, 65, 9)], np.int32)
+    straight = P.Operator(prob, form=form, receivers=rec)
+    rs = straight.apply(24, 0)
+    first = P.Operator(prob, form=form, receivers=rec)
+    first.apply(11, 0)
+    P.write_checkpoint(str(tmp_path), "ck", first)
+    second = P.Operator(prob, form=form, receivers=rec)
+    second.restore(str(tmp_path), "ck", 11)
+    r2 = second.apply(13)
+    nl = 24 % 3
+    assert np.array_equal(second.get_level(nl), straight.get_level(nl))
+    assert np.array_equal(second.get_level((24 + 2) % 3), straight.get_level((24 + 2) % 3))
+    assert np.array_equal(r2.rec_traces, rs.rec_traces[11:])
