@@ -707,10 +707,30 @@ int swb_apply_async(swb_handle* h, int step0, int nt) {
     if (nt > 0) SWB_CUDA(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned) * nt, h->stream));
     h->launches = 0;
     h->ctl.smax = h->d_smax;
-    SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
-    rc = enqueue_steps(h, step0, nt);
-    if (rc) return rc;
-    SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+    // SWB_GRAPH=1: capture the step loop into a CUDA graph (programmatic edges kept) and launch
+    // it as one unit; the capture/instantiation is host work outside the timed events.
+    // Single-domain, single-step launches only (K3 epochs and slab counters are host state).
+    static const bool use_graph = std::getenv("SWB_GRAPH") != nullptr;
+    if (use_graph && !linked(h) && !use_tb(h) && nt > 0) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        SWB_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_steps(h, step0, nt);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+        if (rc) return rc;
+        SWB_CUDA(e);
+        SWB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+        SWB_CUDA(cudaGraphLaunch(exec, h->stream));
+        SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+        cudaGraphExecDestroy(exec);  // released once the launch completes
+        cudaGraphDestroy(graph);
+    } else {
+        SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+        rc = enqueue_steps(h, step0, nt);
+        if (rc) return rc;
+        SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
+    }
     h->pend_step0 = step0;
     h->pend_nt = nt;
     h->pending = true;
