@@ -97,7 +97,16 @@ struct IpcBlob {
     int64_t level_floats;
     cudaIpcMemHandle_t u_handle;
     cudaIpcMemHandle_t flag_handle;
+    unsigned char uuid[16];  // device of the exporting handle
 };
+
+// Fused in-kernel halo ordering needs both slabs' persistent grids resident at once: true on two
+// devices, not when two processes share one GPU (then the wait/signal kernels order the steps).
+bool same_device(int device, const unsigned char* uuid) {
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return false;
+    return std::memcmp(prop.uuid.bytes, uuid, 16) == 0;
+}
 
 }  // namespace
 
@@ -1086,6 +1095,11 @@ int swb_export_ghosts(swb_handle* h, void* blob, size_t* blob_len) {
     b.P2 = h->P2;
     b.H = h->HU;
     b.fused_capable = fused_capable(h) ? 1 : 0;
+    {
+        cudaDeviceProp prop{};
+        SWB_CUDA(cudaGetDeviceProperties(&prop, h->device));
+        std::memcpy(b.uuid, prop.uuid.bytes, 16);
+    }
     b.grid = h->plan.grid;
     b.level_floats = h->level_floats;
     SWB_CUDA(cudaIpcGetMemHandle(&b.u_handle, h->u));
@@ -1117,7 +1131,8 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         for (int l = 0; l < 3; ++l) h->peer.lo_lev[l] = base + l * b.level_floats;
         h->peer.lo_shift = h->xg_off - b.xg_off;
         h->lo_remote = static_cast<unsigned long long*>(h->ipc_lo_f) + 1;
-        h->fused_lo = b.fused_capable && fused_capable(h);
+        h->fused_lo = b.fused_capable && fused_capable(h) &&
+                      (!same_device(h->device, b.uuid) || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
         h->nb_grid_lo = b.grid;
     }
     if (upper_blob && upper_len) {
@@ -1128,7 +1143,8 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         for (int l = 0; l < 3; ++l) h->peer.hi_lev[l] = base + l * b.level_floats;
         h->peer.hi_shift = h->xg_off - b.xg_off;
         h->hi_remote = static_cast<unsigned long long*>(h->ipc_hi_f) + 0;
-        h->fused_hi = b.fused_capable && fused_capable(h);
+        h->fused_hi = b.fused_capable && fused_capable(h) &&
+                      (!same_device(h->device, b.uuid) || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
         h->nb_grid_hi = b.grid;
     }
     h->stats.launch_steps = 1;  // linked slabs step one at a time
