@@ -124,3 +124,50 @@ def test_snapshot_round_trip(tmp_path):
     data, meta = P.read_snapshot(base)
     assert np.array_equal(data, lev[2])
     assert meta == {"shape": (5, 6, 7), "spacing": (10.0, 12.5, 15.0), "step": 12}
+
+
+def _raw_problem(shape=(16, 16, 16), so=4, **kw):
+    p = N.SwbProblem()
+    for d in range(3):
+        p.shape[d] = shape[d]
+        p.spacing[d] = 10.0
+    p.space_order = so
+    p.dt = 0.001
+    m = np.full(shape, 1.0 / 1500.0 ** 2, np.float32)
+    p.m = N.fptr(m)
+    p.form = 0
+    p.time_block = 1
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p, m
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(so=5), "space_order must be an even integer"),
+    (dict(so=26), "space_order above 24"),
+    (dict(shape=(8, 16, 16), so=8), "too small for halo"),
+    (dict(time_block=3), "time_block must be 1"),
+    (dict(form=9), "unknown stencil form"),
+    (dict(dt=0.0), "dt must be positive"),
+    (dict(slab_lo=0, slab_hi=3, so=8), "slab thinner than SO/2 planes"),
+    (dict(slab_lo=10, slab_hi=5), "bad slab range"),
+    (dict(n_receivers=2), "bad receiver list"),
+])
+def test_capi_validation_before_device(kw, msg):
+    """swb_create validates the problem (the reference's std::invalid_argument cases) before it
+    touches a device, so these paths are exercised here without a GPU."""
+    so = kw.pop("so", 4)
+    shape = kw.pop("shape", (16, 16, 16))
+    p, keep = _raw_problem(shape, so, **kw)
+    h = C.c_void_p()
+    rc = N.lib.swb_create(C.byref(p), C.byref(h))
+    assert rc == N.SWB_EINVAL
+    assert msg in N.last_error()
+
+
+def test_capi_null_arguments():
+    h = C.c_void_p()
+    assert N.lib.swb_create(None, C.byref(h)) == N.SWB_EINVAL
+    assert N.lib.swb_destroy(None) == N.SWB_OK
+    assert N.lib.swb_apply(None, 0, 1, None, None, None) == N.SWB_EINVAL
+    assert N.lib.swb_apply_adjoint(None, 1, None, None, None, None) == N.SWB_EINVAL
