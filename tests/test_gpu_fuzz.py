@@ -58,3 +58,41 @@ def test_random_configuration(seed):
     r3 = op.apply(nt, 0)
     assert np.array_equal(op.levels(), fast.u.data)
     assert np.array_equal(r3.rec_traces, fast.rec_traces)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_slab_decomposition(seed):
+    """Random z-slab cuts (2-4 slabs, each at least SO/2 planes thick) of random problems equal
+    the single domain bit for bit, for the factorised and the plain FP64 kernels."""
+    so, shape, nt, vel, damp, width, src, rec, init = _case(500 + seed)
+    h = so // 2
+    rng = np.random.default_rng(77 + seed)
+    nslab = int(rng.integers(2, 5))
+    cuts = sorted(set(int(c) for c in rng.integers(h, shape[0] - h, size=nslab - 1)))
+    bounds = [0] + cuts + [shape[0]]
+    if any(b - a < h for a, b in zip(bounds[:-1], bounds[1:])):
+        bounds = [0, shape[0] // 2, shape[0]]
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
+                              velocity_field=vel, damp_max=damp, damp_width=width, source_point=src)
+    prob = P.make_wave_problem(cfg)
+    for form in ("factorised", "plain_f64"):
+        whole = P.Operator(prob, form=form)
+        for l in range(3):
+            whole.set_level(l, init[l])
+        wr = whole.apply(nt, 0)
+        ops = [P.Operator(prob, form=form, slab=(bounds[i], bounds[i + 1])) for i in range(len(bounds) - 1)]
+        for o in ops:
+            for l in range(3):
+                o.set_level(l, init[l])
+        for lo, hi in zip(ops[:-1], ops[1:]):
+            P.Operator.link_local(lo, hi)
+        for o in ops:
+            o.apply_async(nt, 0)
+        smax = np.max([o.collect(nt) for o in ops], axis=0)
+        assert np.array_equal(smax, wr.step_max_abs), form
+        for l in range(3):
+            full = np.zeros(shape, np.float32)
+            for o in ops:
+                a, b = o.slab
+                full[a:b] = o.get_level(l)[a:b]
+            assert np.array_equal(full, whole.get_level(l)), (form, l)
