@@ -335,13 +335,21 @@ class Operator:
         # m / damp may be passed precomputed (e.g. pinned host buffers); they must equal
         # problem.m_data() / problem.damp_data().
         m = np.ascontiguousarray(problem.m_data() if m is None else m, np.float32)
-        damp = np.ascontiguousarray(problem.damp_data() if damp is None else damp, np.float32)
-        if m.size != problem.cell_count() or damp.size != problem.cell_count():
-            raise ValueError("m/damp size does not match the grid")
+        if m.size != problem.cell_count():
+            raise ValueError("m size does not match the grid")
         w = rounded_weights(problem.space_order)
-        self._keep += [m, damp, w]
+        self._keep += [m, w]
         p.m = N.fptr(m)
-        p.damp = N.fptr(damp)
+        if float(problem.damp_max) == 0.0:
+            # damp_data() is identically zero (src/wave_model.cpp:25-45 scales by damp_max):
+            # NULL tells the library so -- it zero-fills in HBM instead of copying zeros over PCIe
+            p.damp = N.fptr(None)
+        else:
+            damp = np.ascontiguousarray(problem.damp_data() if damp is None else damp, np.float32)
+            if damp.size != problem.cell_count():
+                raise ValueError("damp size does not match the grid")
+            self._keep.append(damp)
+            p.damp = N.fptr(damp)
         p.weights = N.fptr(w)
         if problem.source is not None:
             wav = np.ascontiguousarray(problem.source.wavelet, np.float32)
