@@ -95,7 +95,9 @@ __device__ __forceinline__ float plain_f32_point(const float* __restrict__ ut, l
     acc = __fsub_rn(acc, __fdiv_rn(__fmul_rn(m, up), dden));
     acc = __fadd_rn(acc, __fdiv_rn(__fmul_rn(__fmul_rn(0.5f, dmp), up), __fmul_rn(dt, I)));
     const long long st[3] = {s0, s1, 1};
-#pragma unroll
+    // (the axes are not unrolled at the widest stencils: all 3(2H+1) hoisted loads would not
+    // fit the register file; the term order is unchanged)
+#pragma unroll(H >= 7 ? 1 : 3)
     for (int d = 0; d < 3; ++d) {
         const float hh = K.h[d];
         const float den = __fmul_rn(__fmul_rn(hh, hh), I);
