@@ -58,6 +58,36 @@ struct Pub {
     int ncw;                  // consumer warps of the CTA
 };
 
+// The dim-2 window of one output float4: w[i] = row[i - A] for the indices the stencil reads,
+// [A - H, A + 4 + H).  The smem row is padded to A >= H floats per side (A a multiple of 4 keeps
+// the centre float4 aligned); only the needed part is loaded, 128-bit where aligned and 64/32-bit
+// at the ends (SO 12: 3 LDS.128 + 2 LDS.64 instead of 5 LDS.128).
+template <int A, int I, int HI, int N>
+__device__ __forceinline__ void window_step(const float* rowc, float (&w)[N]) {
+    if constexpr (I < HI) {
+        if constexpr (I % 4 == 0 && I + 4 <= HI) {
+            const float4 v = *reinterpret_cast<const float4*>(rowc - A + I);
+            w[I] = v.x;
+            w[I + 1] = v.y;
+            w[I + 2] = v.z;
+            w[I + 3] = v.w;
+            window_step<A, I + 4, HI>(rowc, w);
+        } else if constexpr (I % 2 == 0 && I + 2 <= HI) {
+            const float2 v = *reinterpret_cast<const float2*>(rowc - A + I);
+            w[I] = v.x;
+            w[I + 1] = v.y;
+            window_step<A, I + 2, HI>(rowc, w);
+        } else {
+            w[I] = rowc[I - A];
+            window_step<A, I + 1, HI>(rowc, w);
+        }
+    }
+}
+template <int H, int A>
+__device__ __forceinline__ void load_window(const float* rowc, float (&w)[4 + 2 * A]) {
+    window_step<A, A - H, A + 4 + H>(rowc, w);
+}
+
 // Fused epilogue of one output plane: 128-bit stores (plus peer stores into the neighbours'
 // ghost planes, and the source injection with the reference's two roundings), the max|u|
 // fold, and the K3 stage-1 progress publication.
@@ -165,14 +195,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
     for (int i = 0; i < R1; ++i) {
         const float* rowc = pp + i * C::W2;
         float w[4 + 2 * C::A];
-#pragma unroll
-        for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
-            const float4 v = *reinterpret_cast<const float4*>(rowc - C::A + 4 * jj);
-            w[4 * jj] = v.x;
-            w[4 * jj + 1] = v.y;
-            w[4 * jj + 2] = v.z;
-            w[4 * jj + 3] = v.w;
-        }
+        load_window<H, C::A>(rowc, w);
         float2 al = splat(0.f), ah = splat(0.f);
 #pragma unroll
         for (int k = H; k >= 2; --k) {
@@ -320,14 +343,7 @@ __device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item&
     const float* rowc = ucol + sp * (C::UPLANE / 4);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // earlier planes' stores landed
     float w[4 + 2 * C::A];
-#pragma unroll
-    for (int jj = 0; jj < (4 + 2 * C::A) / 4; ++jj) {
-        const float4 v = *reinterpret_cast<const float4*>(rowc - C::A + 4 * jj);
-        w[4 * jj] = v.x;
-        w[4 * jj + 1] = v.y;
-        w[4 * jj + 2] = v.z;
-        w[4 * jj + 3] = v.w;
-    }
+    load_window<H, C::A>(rowc, w);
     float2 al = splat(0.f), ah = splat(0.f);
     // far half of the x-neighbours: k = H .. KB+1 (plane p+H is the one that just arrived)
     constexpr int KB = H / 2;
