@@ -212,7 +212,9 @@ def run_ours(args, rank, world, local):
     if not args.no_sweep:
         for s2 in (4, 8, 12, 16):
             if s2 == so:
-                sweep[f"so{s2}"] = {"gpts": round(value, 2), "frac": roof["frac"]}
+                sweep[f"so{s2}"] = {"gpts": round(value, 2), "frac": roof["frac"],
+                                    "gflops": round(value * FLOPS_AGGRESSIVE[s2], 1),
+                                    "oi_flop_per_byte": round(FLOPS_AGGRESSIVE[s2] / BYTES_PER_POINT, 3)}
                 continue
             p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
                                                          space_order=s2, steps=args.sweep_steps + 16))
@@ -231,7 +233,8 @@ def run_ours(args, rank, world, local):
             g2 = allsum(pl, world) * args.sweep_steps / t2 / 1e9
             sweep[f"so{s2}"] = {"gpts": round(g2, 2),
                                 "frac": round(BYTES_PER_POINT * g2 / world / hbm, 4),
-                                "gflops": round(g2 * FLOPS_AGGRESSIVE[s2], 1)}
+                                "gflops": round(g2 * FLOPS_AGGRESSIVE[s2], 1),
+                                "oi_flop_per_byte": round(FLOPS_AGGRESSIVE[s2] / BYTES_PER_POINT, 3)}
             o2.close()
     # ---- K3 temporal blocking (two steps per launch) vs K1, same protocol (BASELINE config 5's
     # comparison; single domain -- linked slabs exchange halos every step and run K1) ----
