@@ -91,7 +91,7 @@ __device__ __forceinline__ void load_window(const float* rowc, float (&w)[4 + 2 
 // Fused epilogue of one output plane: 128-bit stores (plus peer stores into the neighbours'
 // ghost planes, and the source injection with the reference's two roundings), the max|u|
 // fold, and the K3 stage-1 progress publication.
-template <int R1>
+template <int H, int R1>
 __device__ __forceinline__ void epilogue_store(const float4* out, const float4* mv, int p, const Item& it,
                                                unsigned& mine, float* un, float* lo_peer, float* hi_peer,
                                                const Geo& g, const Coef& K, const Ctl& c, const Peer& pr,
@@ -104,8 +104,14 @@ __device__ __forceinline__ void epilogue_store(const float4* out, const float4* 
         // common path: plain stores (rows past the interior are skipped warp-uniformly)
 #pragma unroll
         for (int i = 0; i < R1; ++i)
-            if (it.rows_ok || it.yt + i < g.y1)
-                store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+            if (it.rows_ok || it.yt + i < g.y1) {
+                // H not a multiple of 4: the interior's z bounds cut a lane on (even-extent) grids,
+                // so take the branch-free predicated stores (compile-time choice per variant)
+                if constexpr (H % 4 != 0)
+                    store_row_pred(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+                else
+                    store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+            }
     } else {
         // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same
         // lane masks) and the source plane (the one injected element is patched first)
@@ -279,7 +285,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
         }
         out[i] = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    epilogue_store<R1>(out, mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+    epilogue_store<H, R1>(out, mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
 }
 
 // ---- K1 with the dim-0 queue in tensor memory (UNR == 0 variants) -----------------------
@@ -477,7 +483,7 @@ __device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item&
         }
         out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    epilogue_store<R1>(&out, &mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+    epilogue_store<H, R1>(&out, &mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
 }
 
 template <int H, int R1, int T1, int SU, int SA, int U>

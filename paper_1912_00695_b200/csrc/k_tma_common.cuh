@@ -172,6 +172,33 @@ __device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned 
     }
 }
 
+// Same, for grids whose interior z bounds cut a float4 lane (z0 or z1 not a multiple of 4):
+// full lanes STG.128, half lanes (masks 0b0011 / 0b1100: even bounds) one STG.64, all as
+// predicated stores with a select-masked max, so the warp holding the edge lane does not take
+// the divergent per-element path every plane (that cost the edge-tile CTAs ~5 % at SO 4 and 12).
+// Other masks (odd bounds) still use per-element stores.
+__device__ __forceinline__ void store_row_pred(float* dst, const float4& o, unsigned zmask, unsigned& mine) {
+    asm volatile(
+        "{\n\t.reg .pred pf, pl, ph;\n\t"
+        "setp.eq.u32 pf, %0, 15;\n\t"
+        "setp.eq.u32 pl, %0, 3;\n\t"
+        "setp.eq.u32 ph, %0, 12;\n\t"
+        "@pf st.global.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
+        "@pl st.global.v2.f32 [%1], {%2, %3};\n\t"
+        "@ph st.global.v2.f32 [%1+8], {%4, %5};\n\t"
+        "}" ::"r"(zmask), "l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)
+        : "memory");
+    if (zmask != 0xFu && zmask != 0x3u && zmask != 0xCu && zmask != 0u) {
+        if (zmask & 1u) dst[0] = o.x;
+        if (zmask & 2u) dst[1] = o.y;
+        if (zmask & 4u) dst[2] = o.z;
+        if (zmask & 8u) dst[3] = o.w;
+    }
+    const unsigned a = (zmask & 1u) ? abs_bits(o.x) : 0u, b = (zmask & 2u) ? abs_bits(o.y) : 0u;
+    const unsigned cc = (zmask & 4u) ? abs_bits(o.z) : 0u, d = (zmask & 8u) ? abs_bits(o.w) : 0u;
+    mine = max(mine, max(max(a, b), max(cc, d)));
+}
+
 // One arrival step of a consumer thread: take plane q's centre values into queue slot U,
 // and (after the 2H warm-up planes) produce output plane p = q - dir*H, whose queue slot is
 // (U - H) mod NQ.  All queue indices are compile-time.
