@@ -146,7 +146,9 @@ int swb_apply_adjoint(swb_handle* h, int nt, const float* rec_data, float* src_t
  * and only before the step that would overwrite the level) and drained to snaps[i]
  * (grid-sized, reference interior layout; pinned memory for full PCIe speed) on a separate
  * copy stream, overlapping the following steps.  n_snaps must equal nt / every; snapshot i is
- * the state after step step0 + (i+1)*every - 1.  Other outputs as swb_apply. */
+ * the state after step step0 + (i+1)*every - 1.  Other outputs as swb_apply.  Linked slabs of
+ * one process driven from several threads need pinned snaps[] buffers: a pageable copy can
+ * block its thread inside the driver while the other slabs still have steps to enqueue. */
 int swb_apply_snapshots(swb_handle* h, int step0, int nt, int every, float* const* snaps, int n_snaps,
                         float* step_max_abs, int32_t* first_bad_step, float* rec_traces);
 

@@ -65,3 +65,46 @@ def test_checkpoint_restart_bitwise(form, tmp_path):
     assert np.array_equal(second.get_level(nl), straight.get_level(nl))
     assert np.array_equal(second.get_level((24 + 2) % 3), straight.get_level((24 + 2) % 3))
     assert np.array_equal(r2.rec_traces, rs.rec_traces[11:])
+
+
+def test_snapshots_on_linked_slabs():
+    """Each slab drains its own planes into the grid-sized snapshot buffers; together they equal
+    the single-domain snapshots."""
+    nt, every = 12, 4
+    prob = _prob(nt=nt)
+    whole = P.Operator(prob)
+    _, ref = whole.apply_snapshots(nt, every, 0)
+    bounds = [0, 13, 24, prob.shape[0]]
+    ops = [P.Operator(prob, slab=(bounds[i], bounds[i + 1])) for i in range(3)]
+    for lo, hi in zip(ops[:-1], ops[1:]):
+        P.Operator.link_local(lo, hi)
+    import threading
+    import torch
+    # pinned buffers: a pageable D2H can block its host thread inside the driver while the other
+    # slabs' threads still have to enqueue the steps it depends on
+    snaps = [torch.zeros(prob.shape, dtype=torch.float32, pin_memory=True).numpy() for _ in range(nt // every)]
+    errs = []
+
+    def run(o):
+        try:
+            o.apply_snapshots(nt, every, 0, out=snaps)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+    th = [threading.Thread(target=run, args=(o,)) for o in ops]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for a, b in zip(snaps, ref):
+        assert np.array_equal(a, b)
+
+
+def test_adjoint_rejects_linked_slabs():
+    prob = _prob(nt=6)
+    rec = np.array([[18, 20, 30]], np.int32)
+    a = P.Operator(prob, receivers=rec, slab=(0, 18))
+    b = P.Operator(prob, receivers=rec, slab=(18, prob.shape[0]))
+    P.Operator.link_local(a, b)
+    with pytest.raises(ValueError):
+        a.apply_adjoint(np.zeros((6, 1), np.float32))
