@@ -6,8 +6,8 @@ sys.path.insert(0, '.')
 import paper_1912_00695_b200 as P
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-marks = [1000, 2000, 5000, 10000]
-for so in (4, 8, 16):
+marks = [int(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["1000", "2000", "5000", "10000"])]
+for so in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["4", "8", "16"])]:
     rng = np.random.default_rng(so)
     shape = (n, n, n)
     vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
