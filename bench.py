@@ -51,14 +51,48 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle-reason sampling DURING the timed region (B200_PROFILING.md clocks
+    line).  NVML (pynvml) is polled every ~2 ms from a thread between start() and stop(), which
+    bracket exactly the timed steps (the step loop blocks in the driver with the GIL released);
+    without pynvml it falls back to nvidia-smi at 100 ms."""
+
+    _REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+                ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.path = None
+        self.thread = None
+        self.samples = []
+        self.nv = None
 
     def start(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nv = (nv, h)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.running = True
+
+            def poll():
+                while self.running:
+                    try:
+                        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                             int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nv = None
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -73,6 +107,20 @@ class Clocks:
         time.sleep(0.3)
 
     def stop(self):
+        if self.nv is not None:
+            self.running = False
+            self.thread.join(timeout=2)
+            nv = self.nv[0]
+            if not self.samples:
+                return None
+            reasons = set()
+            for _, r in self.samples:
+                for name, attr in self._REASONS:
+                    if r & int(getattr(nv, attr, 0)):
+                        reasons.add(name)
+            sm = [c for c, _ in self.samples]
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.smax, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml, 2 ms polling inside the timed region"}
         if self.proc is None:
             return None
         time.sleep(0.2)
@@ -100,7 +148,7 @@ class Clocks:
             return None
         loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
         return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi, 100 ms"}
 
 
 def dist_setup():
