@@ -198,6 +198,15 @@ def traffic_from_profiles(so):
         return None
 
 
+def host_threads():
+    """Host cores this process may use. Passed to the CPU arms explicitly: torchrun exports
+    OMP_NUM_THREADS=1 to every rank, which would otherwise pin the reference to one thread."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def pinned(shape):
     import torch
     return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
@@ -369,11 +378,13 @@ def cpu_baseline(n, so, steps):
     cfg = O.OracleConfig(shape=(n, n, n), space_order=so, steps=steps)
     try:
         if O.ref_available():
-            r = O.ref_run(cfg, threads=0)
-            kind, cores = "reference", O.omp_threads("ref")
+            cores = host_threads()
+            r = O.ref_run(cfg, threads=cores)
+            kind = "reference"
         else:
-            r = O.port_run(cfg, threads=0)
-            kind, cores = "port", O.omp_threads("port")
+            cores = host_threads()
+            r = O.port_run(cfg, threads=cores)
+            kind = "port"
     except Exception as e:  # pragma: no cover
         return {"error": str(e)}
     gp = r["point_updates"] / r["wall_seconds"] / 1e9
@@ -393,10 +404,10 @@ def run_reference(args, rank, world):
     cfg = O.OracleConfig(shape=shape, space_order=so, steps=steps)
     use_ref = O.ref_available()
     fn = O.ref_run if use_ref else O.port_run
-    r = fn(cfg, threads=0)
+    cores = host_threads()
+    r = fn(cfg, threads=cores)
     gp = r["point_updates"] / r["wall_seconds"] / 1e9
     kind = "reference" if use_ref else "port"
-    cores = O.omp_threads("ref" if use_ref else "port")
     res = {
         "metric": METRIC, "value": round(gp, 6), "unit": "GPts/s", "n_gpus": world, "steps": steps,
         "warmup": 0, "ms_per_step": round(r["wall_seconds"] * 1e3 / steps, 3), "higher_is_better": True,
