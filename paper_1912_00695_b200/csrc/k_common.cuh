@@ -17,6 +17,17 @@ __device__ __forceinline__ T pick3(T a, T b, T c, int i) {
 
 __device__ __forceinline__ unsigned abs_bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 
+// mine = max(mine, |x|, |y|, |z|, |w|) on the max|u| bits: two FMNMX3.NAN with |.| source
+// modifiers instead of four masks and three integer max.  For non-NaN values this is the
+// integer max of abs_bits (non-negative floats order like their bits); any NaN gives NaN,
+// which is still above +inf as bits.
+__device__ __forceinline__ unsigned fold_abs4(unsigned mine, float x, float y, float z, float w) {
+    float r, r2;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(fabsf(x)), "f"(fabsf(y)), "f"(__uint_as_float(mine)));
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r2) : "f"(fabsf(z)), "f"(fabsf(w)), "f"(r));
+    return __float_as_uint(r2);
+}
+
 // Block-wide max of `mine`, then one conditional atomicMax per block into *dst.
 // Non-negative floats order like their bit patterns; |NaN| > +inf in that order, so a
 // non-finite cell always wins and the host maps bits >= 0x7f800000 to NaN

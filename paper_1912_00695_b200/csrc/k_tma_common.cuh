@@ -160,15 +160,14 @@ __device__ __forceinline__ unsigned zmask_of(int zc, int z0, int z1) {
 __device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned zmask, unsigned& mine) {
     if (zmask == 0xFu) {
         *reinterpret_cast<float4*>(dst) = o;
-        mine = max(mine, max(max(abs_bits(o.x), abs_bits(o.y)), max(abs_bits(o.z), abs_bits(o.w))));
+        mine = fold_abs4(mine, o.x, o.y, o.z, o.w);
     } else if (zmask) {
         if (zmask & 1u) dst[0] = o.x;
         if (zmask & 2u) dst[1] = o.y;
         if (zmask & 4u) dst[2] = o.z;
         if (zmask & 8u) dst[3] = o.w;
-        const unsigned a = (zmask & 1u) ? abs_bits(o.x) : 0u, b = (zmask & 2u) ? abs_bits(o.y) : 0u;
-        const unsigned cc = (zmask & 4u) ? abs_bits(o.z) : 0u, d = (zmask & 8u) ? abs_bits(o.w) : 0u;
-        mine = max(mine, max(max(a, b), max(cc, d)));
+        mine = fold_abs4(mine, (zmask & 1u) ? o.x : 0.f, (zmask & 2u) ? o.y : 0.f, (zmask & 4u) ? o.z : 0.f,
+                         (zmask & 8u) ? o.w : 0.f);
     }
 }
 
@@ -194,9 +193,8 @@ __device__ __forceinline__ void store_row_pred(float* dst, const float4& o, unsi
         if (zmask & 4u) dst[2] = o.z;
         if (zmask & 8u) dst[3] = o.w;
     }
-    const unsigned a = (zmask & 1u) ? abs_bits(o.x) : 0u, b = (zmask & 2u) ? abs_bits(o.y) : 0u;
-    const unsigned cc = (zmask & 4u) ? abs_bits(o.z) : 0u, d = (zmask & 8u) ? abs_bits(o.w) : 0u;
-    mine = max(mine, max(max(a, b), max(cc, d)));
+    mine = fold_abs4(mine, (zmask & 1u) ? o.x : 0.f, (zmask & 2u) ? o.y : 0.f, (zmask & 4u) ? o.z : 0.f,
+                     (zmask & 8u) ? o.w : 0.f);
 }
 
 // One arrival step of a consumer thread: take plane q's centre values into queue slot U,
