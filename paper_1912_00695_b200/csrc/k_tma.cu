@@ -92,19 +92,15 @@ __device__ __forceinline__ void load_window(const float* rowc, float (&w)[4 + 2 
 // ghost planes, and the source injection with the reference's two roundings), the max|u|
 // fold, and the K3 stage-1 progress publication.
 template <int H, int R1>
-__device__ __forceinline__ void epilogue_store(const float4* out, const float4* mv, int p, const Item& it,
-                                               unsigned& mine, float* un, float* lo_peer, float* hi_peer,
-                                               const Geo& g, const Coef& K, const Ctl& c, const Peer& pr,
-                                               const Pub& pub, int j) {
-    const long long xoff = static_cast<long long>(p) * g.plane + it.gcol;
-    const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
-    const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
-    const bool src_plane = c.has_src && p == c.src_x;
-    if (!(lo_m || hi_m || src_plane)) {
+__device__ __forceinline__ void epilogue_store(const float4* out, const float4* mv, int p, long long xoff,
+                                               const Item& it, unsigned& mine, float* un, float* lo_peer,
+                                               float* hi_peer, const Geo& g, const Coef& K, const Ctl& c,
+                                               const Peer& pr, const Pub& pub, int j) {
+    if (static_cast<unsigned>(p - it.s0) >= it.sn) {
         // common path: plain stores (rows past the interior are skipped warp-uniformly)
 #pragma unroll
         for (int i = 0; i < R1; ++i)
-            if (it.rows_ok || it.yt + i < g.y1) {
+            if ((it.rowmask >> i) & 1u) {
                 // H not a multiple of 4: the interior's z bounds cut a lane on (even-extent) grids,
                 // so take the branch-free predicated stores (compile-time choice per variant)
                 if constexpr (H % 4 != 0)
@@ -115,6 +111,9 @@ __device__ __forceinline__ void epilogue_store(const float4* out, const float4* 
     } else {
         // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same
         // lane masks) and the source plane (the one injected element is patched first)
+        const bool lo_m = p >= pr.lo_first && p < pr.lo_last;
+        const bool hi_m = p >= pr.hi_first && p < pr.hi_last;
+        const bool src_plane = c.has_src && p == c.src_x;
 #pragma unroll
         for (int i = 0; i < R1; ++i) {
             const int y = it.yt + i;
@@ -172,7 +171,7 @@ __device__ __forceinline__ void epilogue_store(const float4* out, const float4* 
 }
 
 template <int H, int R1, int T1, int SU, int SA, int QN, int U>
-__device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const Item& it,
+__device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& it,
                                               const float* ucol, const float* acol,
                                               const unsigned* aflag, unsigned full_u,
                                               unsigned empty_u, unsigned full_a, unsigned empty_a,
@@ -285,7 +284,17 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, const 
         }
         out[i] = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    epilogue_store<H, R1>(out, mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+    // output offset p * plane + gcol: kept running (one 64-bit add per plane instead of the
+    // multiply-add), except at SO 12, whose 15-warp variant is at its register cap and spills
+    // with the two extra registers (measured: SO 16 +2.7 %, SO 12 -1.3 % with it)
+    long long xoff;
+    if constexpr (H != 6) {
+        xoff = it.xrun;
+        it.xrun += it.dir > 0 ? g.plane : -g.plane;
+    } else {
+        xoff = static_cast<long long>(p) * g.plane + it.gcol;
+    }
+    epilogue_store<H, R1>(out, mv, p, xoff, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
 }
 
 // ---- K1 with the dim-0 queue in tensor memory (UNR == 0 variants) -----------------------
@@ -483,12 +492,13 @@ __device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item&
         }
         out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    epilogue_store<H, R1>(&out, &mv, p, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+    epilogue_store<H, R1>(&out, &mv, p, static_cast<long long>(p) * g.plane + it.gcol, it, mine, un, lo_peer,
+                          hi_peer, g, K, c, pr, pub, j);
 }
 
 template <int H, int R1, int T1, int SU, int SA, int U>
 struct Unrolled {
-    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + 1], int jb, const Item& it,
+    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + 1], int jb, Item& it,
                                                const float* ucol, const float* acol,
                                                const unsigned* aflag, unsigned full_u, unsigned empty_u,
                                                unsigned full_a, unsigned empty_a, unsigned& su,
@@ -508,7 +518,7 @@ struct Unrolled {
 };
 template <int H, int R1, int T1, int SU, int SA>
 struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
-    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + 1], int, const Item&,
+    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + 1], int, Item&,
                                                const float*, const float*, const unsigned*, unsigned,
                                                unsigned, unsigned, unsigned, unsigned&, unsigned&,
                                                unsigned&, unsigned&, unsigned&, unsigned&, float*,
@@ -518,7 +528,7 @@ struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
 
 template <int H, int R1, int T1, int SU, int SA, int UNR, int U>
 struct ShiftBlock {
-    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + UNR], int jb, const Item& it,
+    __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + UNR], int jb, Item& it,
                                                const float* ucol, const float* acol,
                                                const unsigned* aflag, unsigned full_u, unsigned empty_u,
                                                unsigned full_a, unsigned empty_a, unsigned& su,
@@ -538,7 +548,7 @@ struct ShiftBlock {
 };
 template <int H, int R1, int T1, int SU, int SA, int UNR>
 struct ShiftBlock<H, R1, T1, SU, SA, UNR, UNR> {
-    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + UNR], int, const Item&, const float*,
+    __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + UNR], int, Item&, const float*,
                                                const float*, const unsigned*, unsigned, unsigned, unsigned,
                                                unsigned, unsigned&, unsigned&, unsigned&, unsigned&,
                                                unsigned&, unsigned&, float*, float*, float*, const Geo&,
@@ -786,7 +796,27 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             it.zfull = it.zc >= sc.z0 && it.zc + 3 < sc.z1;
             it.zmask = zmask_of(it.zc, sc.z0, sc.z1);
             it.rows_ok = it.yt + R1 - 1 < sc.y1;
+            it.rowmask = 0u;
+#pragma unroll
+            for (int i = 0; i < R1; ++i) it.rowmask |= (it.yt + i < sc.y1) ? (1u << i) : 0u;
+            {
+                // one range covering the item's special planes (the epilogue re-tests them exactly)
+                int s_lo = it.xb, s_hi = it.xa;
+                const int ra[3] = {pr.lo_first, pr.hi_first, c.has_src ? c.src_x : 0};
+                const int rb[3] = {pr.lo_last, pr.hi_last, c.has_src ? c.src_x + 1 : 0};
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const int a = max(ra[r], it.xa), b = min(rb[r], it.xb);
+                    if (a < b) {
+                        s_lo = min(s_lo, a);
+                        s_hi = max(s_hi, b);
+                    }
+                }
+                it.s0 = s_lo;
+                it.sn = s_lo < s_hi ? static_cast<unsigned>(s_hi - s_lo) : 0u;
+            }
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
+            it.xrun = static_cast<long long>(it.q0 + it.dir * H) * g.plane + it.gcol;  // first output plane
             sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
             if (c.trace && ct == 0 && item == first) {
                 // time when the first output plane's data is complete (end of warm-up)

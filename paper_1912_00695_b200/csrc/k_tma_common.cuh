@@ -142,8 +142,12 @@ __device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {
 struct Item {
     int xa, xb, dir, q0, nq, yt, zc;
     bool zfull, rows_ok;
-    unsigned zmask;  // bit e set: element zc+e lies in the updated z range
+    unsigned zmask;    // bit e set: element zc+e lies in the updated z range
+    unsigned rowmask;  // bit i set: tile row yt+i lies in the updated y range
+    int s0;            // [s0, s0+sn): planes of the item whose epilogue is not the plain store
+    unsigned sn;       // (slab-boundary planes, the source plane; one covering range)
     long long gcol;
+    long long xrun;   // offset of the next output plane's element (running, K1 register queue)
 };
 
 // Per-lane validity mask of the float4 at zc against the updated range [z0, z1).
