@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <map>
 #include <mutex>
@@ -111,6 +112,8 @@ bool same_device(int device, const unsigned char* uuid) {
 }  // namespace
 
 struct swb_handle {
+    // small device buffers (sizes kept for the pool): see hbuf_alloc
+    std::vector<std::pair<void*, size_t>> hbufs;
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -189,14 +192,48 @@ int setup_device(int device) {
         return fail(SWB_ECUDA, std::string("no CUDA device available (") +
                                    cudaGetErrorString(e) + "); there is no CPU fallback");
     if (device < 0 || device >= count) return fail(SWB_EINVAL, "device ordinal out of range");
-    cudaDeviceProp prop{};
-    SWB_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10)
-        return fail(SWB_ECUDA, std::string("device ") + prop.name + " is sm_" +
-                                   std::to_string(prop.major * 10 + prop.minor) +
-                                   "; this library is built for sm_100a (B200) only");
+    // architecture check once per device: two attribute queries (cudaGetDeviceProperties
+    // costs milliseconds, which every handle creation would pay)
+    static std::atomic<unsigned long long> checked{0};
+    const unsigned long long bit = device < 64 ? (1ull << device) : 0ull;
+    if (!(checked.load() & bit)) {
+        int major = 0, minor = 0;
+        SWB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        SWB_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+        if (major != 10) {
+            cudaDeviceProp prop{};
+            SWB_CUDA(cudaGetDeviceProperties(&prop, device));
+            return fail(SWB_ECUDA, std::string("device ") + prop.name + " is sm_" +
+                                       std::to_string(major * 10 + minor) +
+                                       "; this library is built for sm_100a (B200) only");
+        }
+        checked.fetch_or(bit);
+    }
     SWB_CUDA(cudaSetDevice(device));
     return SWB_OK;
+}
+
+// Small per-handle device buffers come from the same pool as the fields, so repeated handles
+// of one problem (the bench's end-to-end runs, a solver re-creating operators) pay no
+// cudaMalloc/cudaFree; the sizes are kept for pool_free in swb_destroy.
+cudaError_t hbuf_alloc(swb_handle* h, void** ptr, size_t bytes) {
+    cudaError_t e = pool_alloc(h->device, ptr, bytes);
+    if (e == cudaSuccess) h->hbufs.emplace_back(*ptr, bytes);
+    return e;
+}
+template <typename T>
+cudaError_t hbuf_alloc(swb_handle* h, T** ptr, size_t bytes) {
+    return hbuf_alloc(h, reinterpret_cast<void**>(ptr), bytes);
+}
+void hbuf_free(swb_handle* h, void* ptr) {
+    if (!ptr) return;
+    for (auto it = h->hbufs.begin(); it != h->hbufs.end(); ++it)
+        if (it->first == ptr) {
+            pool_free(h->device, ptr, it->second);
+            h->hbufs.erase(it);
+            return;
+        }
+    cudaFree(ptr);
 }
 
 void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
@@ -226,10 +263,11 @@ void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
 
 int ensure_smax(swb_handle* h, int nt) {
     if (nt <= h->smax_cap) return SWB_OK;
-    if (h->d_smax) cudaFree(h->d_smax);
+    if (h->d_smax) SWB_CUDA(cudaStreamSynchronize(h->stream));
+    hbuf_free(h, h->d_smax);
     h->d_smax = nullptr;
     int cap = std::max(nt, 1024);
-    SWB_CUDA(cudaMalloc(&h->d_smax, sizeof(unsigned) * cap));
+    SWB_CUDA(hbuf_alloc(h, &h->d_smax, sizeof(unsigned) * cap));
     h->smax_cap = cap;
     return SWB_OK;
 }
@@ -239,9 +277,10 @@ int ensure_traces(swb_handle* h, int nt) {
     if (owned == 0) return SWB_OK;
     long long need = static_cast<long long>(nt) * owned;
     if (need <= h->traces_cap) return SWB_OK;
-    if (h->d_traces) cudaFree(h->d_traces);
+    if (h->d_traces) SWB_CUDA(cudaStreamSynchronize(h->stream));
+    hbuf_free(h, h->d_traces);
     h->d_traces = nullptr;
-    SWB_CUDA(cudaMalloc(&h->d_traces, sizeof(float) * need));
+    SWB_CUDA(hbuf_alloc(h, &h->d_traces, sizeof(float) * need));
     h->traces_cap = static_cast<int>(need);
     return SWB_OK;
 }
@@ -476,10 +515,10 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     SWB_CUDA_C(cudaMemsetAsync(h->u, 0, sizeof(float) * 3 * h->level_floats, h->stream));
     SWB_CUDA_C(cudaMemsetAsync(h->m, 0, sizeof(float) * h->level_floats, h->stream));
     SWB_CUDA_C(cudaMemsetAsync(h->damp, 0, sizeof(float) * h->level_floats, h->stream));
-    SWB_CUDA_C(cudaMalloc(&h->d_ring, 3 * sizeof(unsigned)));
-    SWB_CUDA_C(cudaMalloc(&h->d_flags, 2 * sizeof(unsigned long long)));
+    SWB_CUDA_C(hbuf_alloc(h, &h->d_ring, 3 * sizeof(unsigned)));
+    SWB_CUDA_C(hbuf_alloc(h, &h->d_flags, 2 * sizeof(unsigned long long)));
     SWB_CUDA_C(cudaMemsetAsync(h->d_flags, 0, 2 * sizeof(unsigned long long), h->stream));
-    SWB_CUDA_C(cudaMalloc(&h->d_err, sizeof(unsigned)));
+    SWB_CUDA_C(hbuf_alloc(h, &h->d_err, sizeof(unsigned)));
     SWB_CUDA_C(cudaMemsetAsync(h->d_err, 0, sizeof(unsigned), h->stream));
 
     mark("malloc+memset");
@@ -531,7 +570,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     c.has_src = 0;
     if (p->has_source) {
         h->wavelet_len = p->wavelet_len;
-        SWB_CUDA_C(cudaMalloc(&h->d_wavelet, sizeof(float) * p->wavelet_len));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_wavelet, sizeof(float) * p->wavelet_len));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_wavelet, p->wavelet, sizeof(float) * p->wavelet_len,
                                    cudaMemcpyHostToDevice, h->stream));
         if (p->source[0] >= lo && p->source[0] < hi) {
@@ -612,11 +651,11 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             const double mm = p->m[gi], dd = p->damp ? p->damp[gi] : 0.0;
             iw[q] = rw[q] / (mm + 0.5 * dd * dtd);
         }
-        SWB_CUDA_C(cudaMalloc(&h->d_inj_w, sizeof(double) * iw.size()));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_inj_w, sizeof(double) * iw.size()));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_inj_w, iw.data(), sizeof(double) * iw.size(), cudaMemcpyHostToDevice,
                                    h->stream));
-        SWB_CUDA_C(cudaMalloc(&h->d_rec_idx, sizeof(long long) * ridx.size()));
-        SWB_CUDA_C(cudaMalloc(&h->d_rec_w, sizeof(double) * rw.size()));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_rec_idx, sizeof(long long) * ridx.size()));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_rec_w, sizeof(double) * rw.size()));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_idx, ridx.data(), sizeof(long long) * ridx.size(),
                                    cudaMemcpyHostToDevice, h->stream));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_rec_w, rw.data(), sizeof(double) * rw.size(), cudaMemcpyHostToDevice,
@@ -631,8 +670,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         std::vector<double> sw(8, 0.0);
         si[0] = local_index(p->source[0], p->source[1], p->source[2]);
         sw[0] = ((dtd * dtd) * (mm + 0.5 * dd * dtd)) / mm;
-        SWB_CUDA_C(cudaMalloc(&h->d_src_idx, sizeof(long long) * 8));
-        SWB_CUDA_C(cudaMalloc(&h->d_src_w, sizeof(double) * 8));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_src_idx, sizeof(long long) * 8));
+        SWB_CUDA_C(hbuf_alloc(h, &h->d_src_w, sizeof(double) * 8));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_src_idx, si.data(), sizeof(long long) * 8, cudaMemcpyHostToDevice, h->stream));
         SWB_CUDA_C(cudaMemcpyAsync(h->d_src_w, sw.data(), sizeof(double) * 8, cudaMemcpyHostToDevice, h->stream));
     }
@@ -646,13 +685,13 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         if (h->plan.ok && h->K.iso) {
             SWB_CUDA_C(tma_make_maps(h->plan, g, h->nl0, h->maps));
             const size_t nflags = static_cast<size_t>(h->plan.columns) * std::max(0, g.x1 - g.x0);
-            SWB_CUDA_C(cudaMalloc(&h->d_dflag, std::max<size_t>(nflags, 1)));
+            SWB_CUDA_C(hbuf_alloc(h, &h->d_dflag, std::max<size_t>(nflags, 1)));
             SWB_CUDA_C(cudaMemsetAsync(h->d_dflag, 0, std::max<size_t>(nflags, 1), h->stream));
             if (p->damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
             h->plan.dflag = h->d_dflag;
             h->use_tma = true;
             if (h->time_block >= 2 && h->plan.tb_ok) {
-                SWB_CUDA_C(cudaMalloc(&h->d_tbcnt, sizeof(unsigned long long) * h->plan.tb_items));
+                SWB_CUDA_C(hbuf_alloc(h, &h->d_tbcnt, sizeof(unsigned long long) * h->plan.tb_items));
                 SWB_CUDA_C(cudaMemsetAsync(h->d_tbcnt, 0, sizeof(unsigned long long) * h->plan.tb_items, h->stream));
             }
         }
@@ -1007,14 +1046,11 @@ int swb_destroy(swb_handle* h) {
     pool_free(h->device, h->u, sizeof(float) * 3 * h->level_floats, h->exported);
     pool_free(h->device, h->m, sizeof(float) * h->level_floats);
     pool_free(h->device, h->damp, sizeof(float) * h->level_floats);
-    for (void* q : {static_cast<void*>(h->d_wavelet), static_cast<void*>(h->d_smax),
-                    static_cast<void*>(h->d_ring), static_cast<void*>(h->d_rec_idx),
-                    static_cast<void*>(h->d_rec_w),
-                    static_cast<void*>(h->d_traces), static_cast<void*>(h->d_flags),
-                    static_cast<void*>(h->d_dflag), static_cast<void*>(h->d_err),
-                    static_cast<void*>(h->d_tbcnt), static_cast<void*>(h->d_inj_w),
-                    static_cast<void*>(h->d_src_idx), static_cast<void*>(h->d_src_w),
-                    static_cast<void*>(h->d_adj), static_cast<void*>(h->d_src_trace),
+    // (the step counters are IPC-exported with u: never recycled either)
+    for (const auto& b : h->hbufs)
+        pool_free(h->device, b.first, b.second, h->exported && b.first == static_cast<void*>(h->d_flags));
+    h->hbufs.clear();
+    for (void* q : {static_cast<void*>(h->d_adj), static_cast<void*>(h->d_src_trace),
                     static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
     if (h->s_d2h) cudaStreamSynchronize(h->s_d2h);
