@@ -227,3 +227,41 @@ def test_offgrid_receivers_trilinear(form):
         assert rel_l2(got, ref["coord_traces"]) <= TOL
     with pytest.raises(ValueError, match="outside the grid"):
         P.Operator(P.make_wave_problem(cfg), receiver_coords=[[-1.0, 5.0, 5.0]])
+
+
+@pytest.mark.parametrize("time_block", [1, 2])
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_detected_by_fused_max(so, bad, time_block):
+    """The factorised kernels fold max|u| in their epilogue (FMNMX3.NAN on |u|); a non-finite
+    value must surface as InstabilityError at the first step whose newest level holds it, as
+    max_abs_interior does (src/executor.cpp:526-544, 588-593).  A NaN/inf placed in the
+    interior of u[t] reaches u[t+1] at step 0 through the stencil."""
+    shape = (40, 42, 70)
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
+                                                   space_order=so, steps=6))
+    op = P.Operator(prob, form="factorised", time_block=time_block)
+    u0 = np.zeros(shape, np.float32)
+    u0[20, 21, 33] = bad
+    op.set_level(0, u0)
+    with pytest.raises(P.InstabilityError) as ei:
+        op.apply(4, 0)
+    assert ei.value.step() == 0
+    op.close()
+
+
+@pytest.mark.parametrize("so", [4, 16])
+def test_nonfinite_in_ring_detected(so):
+    """A non-finite value in the never-written ring of the level that becomes newest at step 0
+    is found through the precomputed ring max (k_ring_max), not the stencil epilogue."""
+    shape = (30, 32, 40)
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
+                                                   space_order=so, steps=4))
+    op = P.Operator(prob, form="factorised")
+    u1 = np.zeros(shape, np.float32)
+    u1[0, 5, 7] = np.nan  # plane 0 lies in the ring for every SO
+    op.set_level(1, u1)  # level (0 + 1) % 3: the newest after step 0
+    with pytest.raises(P.InstabilityError) as ei:
+        op.apply(2, 0)
+    assert ei.value.step() == 0
+    op.close()
