@@ -96,3 +96,48 @@ def test_random_slab_decomposition(seed):
                 a, b = o.slab
                 full[a:b] = o.get_level(l)[a:b]
             assert np.array_equal(full, whole.get_level(l)), (form, l)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_fused_slab_exchange(seed, monkeypatch):
+    """Random z-slab cuts with the fused in-kernel halo ordering (TMA producers wait on the
+    neighbours' step counters before loading ghost planes; peer stores of boundary planes; no
+    ordering kernels), forced on one GPU with every slab's grid capped so all persistent CTAs
+    are co-resident, as they are on separate GPUs.  N slabs == 1 domain bit for bit."""
+    so, shape, nt, vel, damp, width, src, rec, init = _case(900 + seed)
+    h = so // 2
+    rng = np.random.default_rng(313 + seed)
+    nslab = int(rng.integers(2, 5))
+    cuts = sorted(set(int(c) for c in rng.integers(h, shape[0] - h, size=nslab - 1)))
+    bounds = [0] + cuts + [shape[0]]
+    if any(b - a < h for a, b in zip(bounds[:-1], bounds[1:])):
+        bounds = [0, shape[0] // 2, shape[0]]
+    cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
+                              velocity_field=vel, damp_max=damp, damp_width=width, source_point=src)
+    prob = P.make_wave_problem(cfg)
+    whole = P.Operator(prob)
+    for l in range(3):
+        whole.set_level(l, init[l])
+    wr = whole.apply(nt, 0)
+    monkeypatch.setenv("SWB_FUSED_SAME_DEVICE", "1")
+    monkeypatch.setenv("SWB_MAX_CTAS", str(148 // (len(bounds) - 1)))
+    ops = [P.Operator(prob, slab=(bounds[i], bounds[i + 1])) for i in range(len(bounds) - 1)]
+    for o in ops:
+        for l in range(3):
+            o.set_level(l, init[l])
+    for lo, hi in zip(ops[:-1], ops[1:]):
+        P.Operator.link_local(lo, hi)
+    for o in ops:
+        o.apply_async(nt, 0)
+    smax = np.max([o.collect(nt) for o in ops], axis=0)
+    # fused ordering: one stencil launch per step and slab, no wait/signal kernels (a slab with
+    # no updatable plane has no TMA plan and its sides fall back to ordering kernels)
+    if all(max(a, h) < min(b, shape[0] - h) for a, b in zip(bounds[:-1], bounds[1:])):
+        assert all(o.stats().kernel_launches == nt for o in ops)
+    assert np.array_equal(smax, wr.step_max_abs)
+    for l in range(3):
+        full = np.zeros(shape, np.float32)
+        for o in ops:
+            a, b = o.slab
+            full[a:b] = o.get_level(l)[a:b]
+        assert np.array_equal(full, whole.get_level(l)), l
