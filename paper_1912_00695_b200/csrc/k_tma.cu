@@ -92,7 +92,7 @@ __device__ __forceinline__ void load_window(const float* rowc, float (&w)[4 + 2 
 // ghost planes, and the source injection with the reference's two roundings), the max|u|
 // fold, and the K3 stage-1 progress publication.
 template <int H, int R1>
-__device__ __forceinline__ void epilogue_store(const float4* out, const float4* mv, int p, long long xoff,
+__device__ __forceinline__ void epilogue_store(const float4* out, int p, long long xoff,
                                                const Item& it, unsigned& mine, float* un, float* lo_peer,
                                                float* hi_peer, const Geo& g, const Coef& K, const Ctl& c,
                                                const Peer& pr, const Pub& pub, int j) {
@@ -121,8 +121,7 @@ __device__ __forceinline__ void epilogue_store(const float4* out, const float4* 
             if (y >= g.y1) continue;
             if (src_plane && y == c.src_y && static_cast<unsigned>(c.src_z - it.zc) < 4u) {
                 const int e = c.src_z - it.zc;
-                set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], comp(mv[i], e),
-                                             static_cast<double>(K.dt)));
+                set_comp(o, e, inject_source(comp(o, e), c.wavelet[c.step], c.src_m, static_cast<double>(K.dt)));
             }
             const long long idx = xoff + static_cast<long long>(i) * g.P2;
             store_row(un + idx, o, it.zmask, mine);
@@ -250,21 +249,20 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     mbar_wait(full_a + 8 * sa, pa_);
     const float* aux = acol + sa * (3 * C::ATILE / 4);
     const bool has_damp = aflag[sa] != 0u;
-    float4 upv[R1], mv[R1], dv[R1];
+    float4 upv[R1], bv[R1], av[R1];
 #pragma unroll
     for (int i = 0; i < R1; ++i) {
         upv[i] = *reinterpret_cast<const float4*>(aux + i * kT2);
-        mv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + i * kT2);
-        dv[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + i * kT2)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + i * kT2);
+        av[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + i * kT2)
+                         : make_float4(1.f, 1.f, 1.f, 1.f);
     }
     mbar_arrive(empty_a + 8 * sa);
     mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
     ring_next<SA>(sa, pa_);
     if (++sp == SU) sp = 0;
-    // ---- combine ----
+    // ---- combine: u+ = u + A (u - u-) + B Lr (dt/h)^2 (coefficient fields, tma_update_coefs) ----
     const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
-    const float2 hdt = splat(K.half_dt);
     float4 out[R1];
 #pragma unroll
     for (int i = 0; i < R1; ++i) {
@@ -274,13 +272,9 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
         for (int h = 0; h < 2; ++h) {
             const float2 ucv = h ? hi2(u0) : lo2(u0);
             const float2 um = h ? hi2(upv[i]) : lo2(upv[i]);
-            const float2 m = h ? hi2(mv[i]) : lo2(mv[i]);
-            const float2 dm = h ? hi2(dv[i]) : lo2(dv[i]);
             const float2 Lr = fma2(R3, ucv, acc[i][h]);
             const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
-            const float2 gg = mul2(dm, hdt);
-            const float2 num = fma2(sub2(m, gg), sub2(ucv, um), Lk);
-            res[h] = add2(ucv, div2(num, add2(m, gg)));
+            res[h] = update2(ucv, um, Lk, h ? hi2(av[i]) : lo2(av[i]), h ? hi2(bv[i]) : lo2(bv[i]));
         }
         out[i] = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
@@ -294,7 +288,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     } else {
         xoff = static_cast<long long>(p) * g.plane + it.gcol;
     }
-    epilogue_store<H, R1>(out, mv, p, xoff, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
+    epilogue_store<H, R1>(out, p, xoff, it, mine, un, lo_peer, hi_peer, g, K, c, pr, pub, j);
 }
 
 // ---- K1 with the dim-0 queue in tensor memory (UNR == 0 variants) -----------------------
@@ -466,15 +460,14 @@ __device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item&
     const float* aux = acol + sa * (3 * C::ATILE / 4);
     const bool has_damp = aflag[sa] != 0u;
     const float4 upv = *reinterpret_cast<const float4*>(aux);
-    const float4 mv = *reinterpret_cast<const float4*>(aux + C::ATILE / 4);
-    const float4 dv = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 bv = *reinterpret_cast<const float4*>(aux + C::ATILE / 4);
+    const float4 av = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2) : make_float4(1.f, 1.f, 1.f, 1.f);
     mbar_arrive(empty_a + 8 * sa);
     mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
     ring_next<SA>(sa, pa_);
     if (++sp == SU) sp = 0;
-    // ---- combine ----
+    // ---- combine (as consumer_step) ----
     const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
-    const float2 hdt = splat(K.half_dt);
     float4 out;
     {
         float2 res[2];
@@ -482,17 +475,13 @@ __device__ __forceinline__ void consumer_step_tq(unsigned tq, int j, const Item&
         for (int h = 0; h < 2; ++h) {
             const float2 ucv = h ? hi2(u0) : lo2(u0);
             const float2 um = h ? hi2(upv) : lo2(upv);
-            const float2 m = h ? hi2(mv) : lo2(mv);
-            const float2 dm = h ? hi2(dv) : lo2(dv);
             const float2 Lr = fma2(R3, ucv, acc[h]);
             const float2 Lk = fma2(Lr, khi, mul2(Lr, klo));
-            const float2 gg = mul2(dm, hdt);
-            const float2 num = fma2(sub2(m, gg), sub2(ucv, um), Lk);
-            res[h] = add2(ucv, div2(num, add2(m, gg)));
+            res[h] = update2(ucv, um, Lk, h ? hi2(av) : lo2(av), h ? hi2(bv) : lo2(bv));
         }
         out = make_float4(res[0].x, res[0].y, res[1].x, res[1].y);
     }
-    epilogue_store<H, R1>(&out, &mv, p, static_cast<long long>(p) * g.plane + it.gcol, it, mine, un, lo_peer,
+    epilogue_store<H, R1>(&out, p, static_cast<long long>(p) * g.plane + it.gcol, it, mine, un, lo_peer,
                           hi_peer, g, K, c, pr, pub, j);
 }
 
@@ -1154,6 +1143,22 @@ cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* out)
 static_assert(sizeof(Maps) == kTmaMapsBytes, "tensor-map block size");
 
 namespace {
+__global__ void k_update_coefs(float* __restrict__ m, float* __restrict__ damp, long long n, float half_dt) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float mf = m[i];
+        const float g = damp[i] * half_dt;  // fl(damp dt/2), as the update has always rounded it
+        float b = 0.f, a = 0.f;
+        if (mf != 0.f) {
+            const double mp = static_cast<double>(mf) + static_cast<double>(g);
+            b = static_cast<float>(1.0 / mp);
+            a = static_cast<float>((static_cast<double>(mf) - static_cast<double>(g)) / mp);
+        }
+        m[i] = b;
+        damp[i] = a;
+    }
+}
+
 // flags[col * np + (x - x0)] = any damp != 0 over the output points of that tile and plane
 __global__ void k_damp_flags(const float* __restrict__ damp, long long plane, int P2, int x0, int np,
                              int y0, int y1, int z0, int z1, int zs, int T1, int tiles_z,
@@ -1170,6 +1175,12 @@ __global__ void k_damp_flags(const float* __restrict__ damp, long long plane, in
     if (threadIdx.x == 0) flags[static_cast<long long>(col) * np + blockIdx.x] = static_cast<unsigned char>(any);
 }
 }  // namespace
+
+cudaError_t tma_update_coefs(float* m, float* damp, long long n, float half_dt, cudaStream_t s) {
+    k_update_coefs<<<148 * 8, 256, 0, s>>>(m, damp, n, half_dt);
+    return cudaGetLastError();
+}
+
 
 cudaError_t tma_damp_flags_device(const TmaPlan& plan, const Geo& g, unsigned char* flags, cudaStream_t s) {
     const int np = g.x1 - g.x0;

@@ -129,6 +129,13 @@ __device__ __forceinline__ float2 div2(float2 n, float2 d) {
     return fma2(e, r, q);
 }
 
+// The time update with the per-point coefficient fields of K1 (tma_update_coefs):
+//   u+ = u + A (u - u-) + B Lk,   A = (m - g)/(m + g),  B = 1/(m + g),  g = damp dt/2,
+// which is u + [(m - g)(u - u-) + Lk]/(m + g) without a division; A = 1 where no damping.
+__device__ __forceinline__ float2 update2(float2 u, float2 um, float2 Lk, float2 a, float2 b) {
+    return fma2(b, Lk, fma2(a, sub2(u, um), u));
+}
+
 // Advance a ring position (stage, phase) by one.
 template <int S>
 __device__ __forceinline__ void ring_next(unsigned& st, unsigned& ph) {

@@ -50,6 +50,9 @@ void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_lo
 // Same flags computed on the device from the uploaded damp field.
 cudaError_t tma_damp_flags_device(const TmaPlan& plan, const Geo& g, unsigned char* flags, cudaStream_t s);
 TmaPlan tma_plan(int H, const Geo& g, int num_sms);
+// In place: m -> B = 1/(m + g), damp -> A = (m - g)/(m + g), g = fl(damp * half_dt), computed in
+// double and rounded once (cells with m == 0, row padding, get 0).  For K1 handles only.
+cudaError_t tma_update_coefs(float* m, float* damp, long long n, float half_dt, cudaStream_t s);
 // Encodes the tensor maps for the three u levels (once per handle).
 constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps
 cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*kTmaMapsBytes*/);

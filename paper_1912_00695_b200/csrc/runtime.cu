@@ -578,6 +578,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             c.src_x = p->source[0] - h->xg_off;
             c.src_y = p->source[1];
             c.src_z = p->source[2];
+            c.src_m = p->m[(static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2]];
         }
     }
     c.wavelet = h->d_wavelet;
@@ -690,6 +691,10 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             if (p->damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
             h->plan.dflag = h->d_dflag;
             h->use_tma = true;
+            // K1 reads m and damp only as the update coefficients B = 1/(m+g), A = (m-g)/(m+g):
+            // transform them in place (after the damp flags above, same stream)
+            if (h->plan.kind == 0)
+                SWB_CUDA_C(tma_update_coefs(h->m, h->damp, h->level_floats, h->K.half_dt, h->stream));
             if (h->time_block >= 2 && h->plan.tb_ok) {
                 SWB_CUDA_C(hbuf_alloc(h, &h->d_tbcnt, sizeof(unsigned long long) * h->plan.tb_items));
                 SWB_CUDA_C(cudaMemsetAsync(h->d_tbcnt, 0, sizeof(unsigned long long) * h->plan.tb_items, h->stream));

@@ -51,6 +51,7 @@ struct Ctl {
     int wavelet_len;
     int has_src;            // source owned by this handle
     int src_x, src_y, src_z;  // LOCAL coordinates of the source
+    float src_m;              // m at the source point (the injection's dt^2 amp / m)
     unsigned* smax;         // [nt] per-step max|u| bits (atomicMax over non-negative floats)
     int step;               // absolute step
     int slot;               // index into smax / traces for this step
