@@ -1,7 +1,8 @@
 // Exercise the drop-in executor exactly as a reference user calls exec::run:
 //   make_wave_problem -> wave_equations -> lower -> optimize_all(dse) -> build_iet -> exec::run
-// Usage: dropin_run <basic|aggressive> <n0> <n1> <n2> <so> <steps> <damp_max> <out.bin>
+// Usage: dropin_run <basic|aggressive> <n0> <n1> <n2> <so> <steps> <damp_max> <out.bin> [dt]
 // Writes: int32 final_level, uint64 point_updates, float step_max_abs[steps], float levels[3][n].
+// Exit codes: 0 ok, 3 exec::InstabilityError (prints the step), 1 other exception.
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -14,8 +15,8 @@
 using namespace stencilc;
 
 int main(int argc, char** argv) {
-    if (argc != 9) {
-        std::fprintf(stderr, "usage: %s dse n0 n1 n2 so steps damp_max out\n", argv[0]);
+    if (argc != 9 && argc != 10) {
+        std::fprintf(stderr, "usage: %s dse n0 n1 n2 so steps damp_max out [dt]\n", argv[0]);
         return 2;
     }
     exec::WaveProblemConfig cfg;
@@ -25,6 +26,7 @@ int main(int argc, char** argv) {
     cfg.steps = std::atoi(argv[6]);
     cfg.damp_max = std::atof(argv[7]);
     cfg.damp_width = 4;
+    if (argc == 10) cfg.dt = std::atof(argv[9]);  // <= 0: the CFL step (the reference default)
     try {
         auto p = exec::make_wave_problem(cfg);
         auto eqs = exec::wave_equations(p);

@@ -41,3 +41,26 @@ def test_reference_api_runs_on_b200(so, damp, tmp_path):
     fl, pu, smax, lv = run_dropin("aggressive", shape, so, steps, damp, tmp_path)
     err = np.linalg.norm(lv[fl] - ref["levels"][fl]) / np.linalg.norm(ref["levels"][fl])
     assert err <= 1e-5
+
+
+@pytest.mark.skipif(not os.path.exists(EXE), reason="drop-in binary not built (needs /root/reference)")
+@pytest.mark.parametrize("dse", ["basic", "aggressive"])
+def test_reference_api_instability_error(dse, tmp_path):
+    """exec::run on the B200 kernels throws exec::InstabilityError with the first non-finite step,
+    as the reference interpreter does (src/executor.cpp:588-593); the basic IET's step equals the
+    C restatement's, and the aggressive IET's the Python mirror's factorised run."""
+    import paper_1912_00695_b200 as P
+    shape, so, steps, dt = (16, 16, 16), 4, 400, 0.02
+    p = subprocess.run([EXE, dse, *map(str, shape), str(so), str(steps), "0", str(tmp_path / "x.bin"), str(dt)],
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode == 3, p.stdout + p.stderr
+    step = int(p.stdout.strip().split("step=")[1])
+    if dse == "basic":
+        with pytest.raises(O.OracleError) as eo:
+            O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=steps, dt=dt))
+        assert step == eo.value.step
+    else:
+        cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=steps, dt=dt)
+        with pytest.raises(P.InstabilityError) as ei:
+            P.run(P.make_wave_problem(cfg), dse=P.DseLevel.aggressive)
+        assert step == ei.value.step()
