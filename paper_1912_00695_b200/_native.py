@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libswb.so")
+LIB_PATH = os.environ.get("SWB_LIB") or os.path.join(_HERE, "_lib", "libswb.so")  # SWB_LIB: development A/B
 
 SWB_OK, SWB_EINVAL, SWB_ECUDA, SWB_EUNSTABLE = 0, 1, 2, 3
 FORM_FACTORISED, FORM_PLAIN_F64, FORM_PLAIN_F32, FORM_FACTORISED_SIMPLE = 0, 1, 2, 3
