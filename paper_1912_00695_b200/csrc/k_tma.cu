@@ -736,7 +736,9 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                         mbar_expect_tx(full_a + 8 * st, (need_damp ? 3 : 2) * C::ATILE);
                         const unsigned dst = aring_s + st * 3 * C::ATILE;
                         tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * st, pol_first);
-                        tma_load3_hint(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * st, pol_first);
+                        // B (1/(m+g)) is re-read every step: default L2 policy (evict_first measured
+                        // -3 % at 512^3 SO 8); u[t-1] and A stay evict_first
+                        tma_load3(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * st);
                         if (need_damp)
                             tma_load3_hint(dst + 2 * C::ATILE, &maps.damp, zt, yt, p, full_a + 8 * st,
                                            pol_first);
