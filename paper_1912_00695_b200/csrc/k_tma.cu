@@ -1,26 +1,28 @@
 // K1: TMA-staged 2.5D factorised stencil for sm_100a.
 //
-// One persistent CTA per SM walks a contiguous, balanced range of (column tile, plane)
-// work: a column tile is T1 rows (dim 1) x 64 cols (dim 2) of output points; the CTA
-// streams it along dim 0 (the reference's slowest axis "x"; the north star's "z-slab"
-// axis).  Warp 0 is the TMA producer; warps 1..NC are consumers.
+// One persistent CTA per SM strides over work items (column tile x dim-0 chunk): a column
+// tile is T1 rows (dim 1) x 64 cols (dim 2) of output points; the CTA streams it along dim 0
+// (the reference's slowest axis "x"; the north star's "z-slab" axis) over the chunk's planes.
+// Warp 0 is the TMA producer (lane 0: u ring, lane 1: aux ring); warps 1..NCW are consumers.
 //
 //   u ring  : halo-padded planes of u[t] ((T1+2H) x (64+2A) floats) loaded by
 //             cp.async.bulk.tensor.3d; a plane stays resident from its arrival (when the
 //             consumers take its centre values into the register queue) until the output
 //             plane with the same index has used it for the in-plane (dim 1 / dim 2) stencil,
 //             H planes later.  Depth S_U = H + 1 + prefetch.
-//   aux ring: u[t-1], m, damp tiles (T1 x 64) of the output plane, one TMA each.
+//   aux ring: u[t-1], B, A tiles (T1 x 64) of the output plane, one TMA each (A only where
+//             the tile is damped); B and A are the coefficient fields that replace m and damp.
 //   register queue: each consumer thread keeps u[t] of its R1 x 4 points for the 2H+1
 //             planes around the output plane (the dim-0 stencil never touches smem).
 //
 // Arithmetic per point (factorised form, src/pipeline.cpp:467-512 with the sign fix):
 //   S  = sum_k>=2 c_k (u_-k + u_+k) over the three axes + c_1 sum((u_-1 - u) + (u_+1 - u))
 //   Lr = S + 3 (c_0 + 2 c_1) u
-//   u+ = u + [ (m - g)(u - u-) + Lr (dt/h)^2 ] / (m + g),   g = damp dt/2
-// (see combine_f32 in k_common.cuh), then the fused epilogue: source injection with the
-// reference's two roundings, 128-bit stores, peer stores of slab-boundary planes, and the
-// per-step max|u| / non-finite flag.
+//   u+ = u + A (u - u-) + B Lr (dt/h)^2,   A = (m - g)/(m + g),  B = 1/(m + g),  g = damp dt/2
+// (update2 in k_tma_common.cuh; the one-thread-per-point kernels divide instead, combine_f32
+// in k_common.cuh), then the fused epilogue: source injection with the reference's two
+// roundings, 128-bit stores, peer stores of slab-boundary planes, and the per-step max|u| /
+// non-finite flag.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
