@@ -22,7 +22,8 @@
  *     *_async; a handle is not re-entrant (like the reference Engine).
  *   - Return codes: SWB_OK, SWB_EINVAL (the reference throws std::invalid_argument),
  *     SWB_ECUDA (device/driver failure), SWB_EUNSTABLE (the reference throws
- *     InstabilityError{step}, include/stencilc/executor.hpp:62-70).  swb_last_error() gives
+ *     InstabilityError{step}, include/stencilc/executor.hpp:62-70), SWB_ERANGE (the reference
+ *     throws std::out_of_range under RunOptions::check_bounds).  swb_last_error() gives
  *     the message of the last failing call on this thread.
  *   - There is no CPU fallback: without a usable sm_100 device swb_create fails with SWB_ECUDA.
  */
@@ -40,14 +41,19 @@ extern "C" {
 #define SWB_EINVAL 1
 #define SWB_ECUDA 2
 #define SWB_EUNSTABLE 3
+#define SWB_ERANGE 4   /* RunOptions::check_bounds: an access leaves the allocation (std::out_of_range) */
 
 /* Stencil form.  The reference has two IETs for the same problem (pipeline::DseLevel,
  * include/stencilc/pipeline.hpp:17; src/pipeline.cpp:467-512):
  *   basic      -> the solved update term by term, 3*SO+3 divisions per point.
  *   aggressive -> factorised/CSE form (its shipped version has a sign bug,
  *                 src/pipeline.cpp:246-248; we implement the corrected algebra).
- * SWB_FORM_FACTORISED : aggressive algebra, FP32 Laplacian (difference form on the k=1 ring)
- *                       with an FP64 final combine.  The production kernel (TMA 2.5D).
+ * SWB_FORM_FACTORISED : aggressive algebra, FP32 Laplacian (difference form on the k=1 ring).
+ *                       The production kernel (TMA 2.5D, isotropic spacing, SO >= 2) combines in
+ *                       FP32 with per-point coefficient fields B = 1/(m+g), A = (m-g)/(m+g),
+ *                       g = damp dt/2 (computed once per handle in FP64, rounded once):
+ *                       u+ = u + A (u - u-) + B Lr (dt/h)^2.  Anisotropic spacing takes the
+ *                       one-thread-per-point fallback with an FP64 final combine.
  * SWB_FORM_PLAIN_F64  : basic form evaluated exactly as the interpreter does (double,
  *                       same term order, one division per product, no FMA): bit-exact.
  * SWB_FORM_PLAIN_F32  : basic form in FP32 term by term (the paper's OPS kernel, src/opsgen.cpp:327-355).
@@ -92,6 +98,14 @@ typedef struct swb_problem {
      * (a,b,c) lexicographic order, of ((wx_a*wy_b)*wz_c)*u in double, w0 = 1-f, w1 = f. */
     int32_t n_coord_receivers;
     const double* coord_receivers;
+    /* RunOptions::check_bounds (include/stencilc/executor.hpp:74; src/executor.cpp:233, 333,
+     * 417-428): validate every access of the operator -- the stencil reach of the update interior,
+     * the source point's u and m accesses, the receivers -- against the reference's padded
+     * allocation (u padded by SO/2, m and damp by 1) before anything runs; the first access
+     * outside fails with SWB_ERANGE and the interpreter's message ("access to u leaves the
+     * allocation in x at step 0").  Without it, a source outside the update interior is
+     * SWB_EINVAL. */
+    int32_t check_bounds;
 } swb_problem;
 
 typedef struct swb_handle swb_handle;
@@ -114,6 +128,11 @@ int swb_set_level(swb_handle* h, int level, const float* grid_sized);
 
 /* Field::interior(level) (src/executor.cpp:56-71) of the current state. */
 int swb_get_level(swb_handle* h, int level, float* grid_sized);
+
+/* Field::level_data(level) filled in place (src/executor.cpp:28-44: halo-padded C-order levels):
+ * the grid-sized level lands at offset `halo` in every dim of a (n0+2h) x (n1+2h) x (n2+2h)
+ * host block; the padding is not touched.  One pitched copy, no host repacking. */
+int swb_get_level_padded(swb_handle* h, int level, float* padded, int halo);
 
 /* The time loop (src/executor.cpp:577-597) for steps step0 .. step0+nt-1; level rotation
  * (step+toff) mod 3 as in resolve_channels (src/executor.cpp:407-415).  Outputs (each

@@ -14,9 +14,16 @@
 // kernel (bit-identical to the interpreter), aggressive -> factorised TMA kernel (the
 // sign-corrected algebra; the reference's own aggressive output is wrong).
 // Any other tree throws std::invalid_argument: there is no CPU fallback.
+//
+// Restated by contract (this file replaces src/executor.cpp wholesale, so the pieces a caller can
+// observe must match it): Field's constructor, cell_index() and at() (src/executor.cpp:29-54,
+// the padded C-order storage every reference caller indexes into) and write_snapshot()
+// (src/executor.cpp:816-837, a byte-identical on-disk format).  Everything else -- IET
+// classification, check_bounds, the C-ABI driving, RunResult assembly -- is new.
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <filesystem>
 #include <fstream>
 #include <limits>
@@ -60,16 +67,19 @@ float Field::at(int level, std::span<const int> point) const {
 
 namespace {
 
-// grid-sized <-> padded copies, rank 3 (the operator's rank)
+// grid-sized <-> padded copies: one memcpy per innermost row (the last dim is unit-stride in
+// both layouts), rows visited in C order
 template <typename F>
-void for_each_interior(const Field& f, F fn) {
+void for_each_interior_row(const Field& f, F fn) {
     const auto& shape = f.function()->grid()->shape();
-    std::vector<int> p(shape.size(), 0);
-    std::size_t n = 1;
-    for (int s : shape) n *= static_cast<std::size_t>(s);
-    for (std::size_t i = 0; i < n; ++i) {
-        fn(i, f.cell_index(p));
-        for (int d = static_cast<int>(shape.size()) - 1; d >= 0; --d) {
+    const size_t rank = shape.size();
+    const std::size_t len = static_cast<std::size_t>(shape[rank - 1]);
+    std::size_t rows = 1;
+    for (size_t d = 0; d + 1 < rank; ++d) rows *= static_cast<std::size_t>(shape[d]);
+    std::vector<int> p(rank, 0);
+    for (std::size_t r = 0; r < rows; ++r) {
+        fn(r * len, f.cell_index(p), len);
+        for (int d = static_cast<int>(rank) - 2; d >= 0; --d) {
             if (++p[d] < shape[d]) break;
             p[d] = 0;
         }
@@ -83,7 +93,9 @@ std::vector<float> Field::interior(int level) const {
     for (int s : fn_->grid()->shape()) n *= static_cast<std::size_t>(s);
     std::vector<float> out(n);
     const float* base = level_data(level);
-    for_each_interior(*this, [&](std::size_t i, std::size_t c) { out[i] = base[c]; });
+    for_each_interior_row(*this, [&](std::size_t i, std::size_t c, std::size_t len) {
+        std::memcpy(out.data() + i, base + c, len * sizeof(float));
+    });
     return out;
 }
 
@@ -92,7 +104,9 @@ void Field::fill_interior(int level, std::span<const float> values) {
     for (int s : fn_->grid()->shape()) n *= static_cast<std::size_t>(s);
     if (values.size() != n) throw std::invalid_argument("interior data size does not match the grid");
     float* base = level_data(level);
-    for_each_interior(*this, [&](std::size_t i, std::size_t c) { base[c] = values[i]; });
+    for_each_interior_row(*this, [&](std::size_t i, std::size_t c, std::size_t len) {
+        std::memcpy(base + c, values.data() + i, len * sizeof(float));
+    });
 }
 
 // --- the operator ----------------------------------------------------------------------
@@ -116,7 +130,107 @@ int classify(const pipeline::IetNodePtr& iet, const WaveProblem& p) {
 void check(int rc) {
     if (rc == SWB_OK) return;
     if (rc == SWB_EINVAL) throw std::invalid_argument(swb_last_error());
+    if (rc == SWB_ERANGE) throw std::out_of_range(swb_last_error());
     throw std::runtime_error(std::string("B200 operator: ") + swb_last_error());
+}
+
+// ---- RunOptions::check_bounds (src/executor.cpp:233, 333, 417-428, 553) ----------------------
+// The interpreter validates every field access of every point against the padded allocation
+// and throws std::out_of_range at the first one that leaves it.  The accesses of an IET are
+// fixed (function, constant offsets) over box-shaped clusters, so the first failing access is
+// found exactly without visiting the points: for each access, the lexicographically first point
+// of the cluster's box where it leaves [-halo, n+halo) in some dim; the earliest such point over
+// the cluster's accesses, ties going to program order (compile_expr's traversal,
+// src/executor.cpp:216-286: add terms in order, numerator then denominator factors; per point
+// the point temps, then each store's update before its target).  Clusters run in IET order and
+// the first step (0) is the first to touch anything.
+struct Access {
+    sym::FunctionPtr fn;
+    std::vector<int> off;
+};
+
+void collect_accesses(const sym::ExprPtr& e, std::vector<Access>& out) {
+    using sym::ExprKind;
+    switch (e->kind) {
+        case ExprKind::indexed:
+            out.push_back({e->function, e->offsets});
+            return;
+        case ExprKind::derivative:
+            throw std::logic_error("tree contains an unexpanded derivative");
+        case ExprKind::add:
+            for (const auto& t : sym::add_terms(e)) collect_accesses(t.term, out);
+            return;
+        case ExprKind::mul:
+        case ExprKind::pow: {
+            const sym::MulParts parts = sym::mul_parts(e);
+            for (const auto& [base, exp] : parts.numerator) collect_accesses(base, out);
+            for (const auto& [base, exp] : parts.denominator) collect_accesses(base, out);
+            return;
+        }
+        default:
+            return;
+    }
+}
+
+void check_cluster(const std::vector<pipeline::Bounds>& box, const std::vector<Access>& acc) {
+    const int rank = static_cast<int>(box.size());
+    std::vector<int> best;
+    int best_i = -1;
+    for (size_t i = 0; i < acc.size(); ++i) {
+        const auto& a = acc[i];
+        const int h = a.fn->halo();
+        const auto& shape = a.fn->grid()->shape();
+        std::vector<int> first(static_cast<size_t>(rank));
+        for (int d = 0; d < rank; ++d) first[d] = box[d].lo;
+        bool fails = false;
+        for (int d = 0; d < rank && !fails; ++d)  // the box's first point already outside?
+            fails = box[d].lo + a.off[d] + h < 0 || box[d].lo + a.off[d] + h >= shape[d] + 2 * h;
+        if (!fails) {
+            // else: the innermost dim whose upper end leaves the allocation, at its first bad value
+            for (int d = rank - 1; d >= 0; --d) {
+                const int last_ok = shape[d] + h - 1 - a.off[d];
+                if (box[d].hi > last_ok) {
+                    first[d] = last_ok + 1;
+                    fails = true;
+                    break;
+                }
+            }
+        }
+        if (fails && (best_i < 0 || first < best)) {
+            best = first;
+            best_i = static_cast<int>(i);
+        }
+    }
+    if (best_i < 0) return;
+    const auto& a = acc[static_cast<size_t>(best_i)];
+    const int h = a.fn->halo();
+    for (int d = 0; d < rank; ++d) {
+        const int idx = best[d] + a.off[d] + h;
+        if (idx < 0 || idx >= a.fn->grid()->shape()[d] + 2 * h)
+            throw std::out_of_range("access to " + a.fn->name() + " leaves the allocation in " +
+                                    a.fn->grid()->space_dims()[d].name + " at step 0");
+    }
+}
+
+void check_bounds(const pipeline::IetNodePtr& node, std::vector<pipeline::Bounds>& box) {
+    using pipeline::IetKind;
+    if (node->kind == IetKind::space_loop) {
+        box.push_back(node->range);
+        for (const auto& c : node->children) check_bounds(c, box);
+        box.pop_back();
+        return;
+    }
+    if (node->kind == IetKind::exprs) {
+        std::vector<Access> acc;
+        for (const auto& b : node->point_temps) collect_accesses(b.value, acc);
+        for (const auto& st : node->stores) {
+            collect_accesses(st.update, acc);
+            collect_accesses(st.target, acc);
+        }
+        check_cluster(box, acc);
+        return;
+    }
+    for (const auto& c : node->children) check_bounds(c, box);
 }
 
 struct Handle {
@@ -149,6 +263,7 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     }
     sp.form = form;
     sp.time_block = 1;
+    sp.check_bounds = options.check_bounds ? 1 : 0;
     Handle h;
     check(swb_create(&sp, &h.h));
     if (options.initial_u) {
@@ -160,6 +275,9 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
         }
     }
     RunResult result{Field(problem.u)};
+    // device level -> the Field's padded storage in place (one pitched copy; the padding keeps
+    // its zeros, as the interpreter never writes it)
+    auto fetch = [&](int l) { check(swb_get_level_padded(h.h, l, result.u.level_data(l), result.u.halo())); };
     const int nt = problem.steps;
     result.step_max_abs.assign(static_cast<size_t>(nt), 0.0f);
     int32_t bad = -1;
@@ -171,27 +289,22 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
                                             " (unstable dt?)");
         check(rc);
     } else {
-        // on_step needs the host field after every step: one step per call (slow path).
-        std::vector<float> lvl(problem.cell_count());
+        // on_step needs the host field after every step: one step per call (slow path).  Step s
+        // writes only level (s+1)%3, so after one full download only the newest level moves.
+        for (int l = 0; l < 3; ++l) fetch(l);
         for (int s = 0; s < nt; ++s) {
             int rc = swb_apply(h.h, s, 1, &result.step_max_abs[static_cast<size_t>(s)], &bad, nullptr);
             if (rc == SWB_EUNSTABLE)
                 throw InstabilityError(bad, "non-finite wave field at step " + std::to_string(bad) +
                                                 " (unstable dt?)");
             check(rc);
-            for (int l = 0; l < 3; ++l) {
-                check(swb_get_level(h.h, l, lvl.data()));
-                result.u.fill_interior(l, lvl);
-            }
+            fetch((s + 1) % 3);
             options.on_step(s, result.u, (s + 1) % 3);
         }
     }
     auto t1 = std::chrono::steady_clock::now();
-    std::vector<float> lvl(problem.cell_count());
-    for (int l = 0; l < 3; ++l) {
-        check(swb_get_level(h.h, l, lvl.data()));
-        result.u.fill_interior(l, lvl);
-    }
+    if (!options.on_step)
+        for (int l = 0; l < 3; ++l) fetch(l);
     result.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
     // point_updates as the interpreter counts them (src/executor.cpp:303-304, 585)
     const int halo = std::max(problem.space_order / 2, 1);
@@ -203,16 +316,29 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     return result;
 }
 
+// check_bounds first: the interpreter would compile and start executing any tree and throw at its
+// first access outside the allocation, before anything could tell it is not the acoustic IET.
+int classify_checked(const pipeline::IetNodePtr& iet, const WaveProblem& p, const RunOptions& options) {
+    if (options.check_bounds) {
+        std::vector<pipeline::Bounds> box;
+        check_bounds(iet, box);
+    }
+    return classify(iet, p);
+}
+
 }  // namespace
 
 RunResult run(const pipeline::IetNodePtr& iet, const WaveProblem& problem, const RunOptions& options) {
-    return execute(problem, options, classify(iet, problem));
+    return execute(problem, options, classify_checked(iet, problem, options));
 }
 
+// executor.hpp:93-96 promises reference_run is bit-identical to run() with threads == 1, so it
+// runs the same kernel as run() for the same tree: basic -> the plain FP64 kernel (bit-identical to
+// the reference interpreter as well), aggressive -> the factorised kernel.  (The reference's own
+// aggressive tree is sign-buggy, src/pipeline.cpp:246-248, so no kernel reproduces it.)
 RunResult reference_run(const pipeline::IetNodePtr& iet, const WaveProblem& problem,
                         const RunOptions& options) {
-    classify(iet, problem);
-    return execute(problem, options, SWB_FORM_PLAIN_F64);  // bit-identical to the interpreter
+    return execute(problem, options, classify_checked(iet, problem, options));
 }
 
 void write_snapshot(const std::string& directory, const std::string& stem, int step, const Field& field,

@@ -1,4 +1,5 @@
-// ORACLE TEST INFRASTRUCTURE ONLY (never linked into the product path).
+// Build fix for the reference's own host code (used by the drop-in build, integration/Makefile,
+// and by the oracle build, oracle/Makefile).
 //
 // Replacement for the reference's src/fd_coefficients.cpp:40-83, which solves
 // the Taylor table over Boost.Multiprecision/Boost.Rational (src/fd_coefficients.cpp:1-2;
@@ -10,7 +11,7 @@
 //   d = 1:  c(+k)  = (-1)^(k+1) p_k / k,      c(-k) = -c(+k),  c(0) = 0
 //
 // The result is checked against an independent Fraction-based Gaussian
-// elimination of the Taylor system in tests/test_oracle_pins.py.
+// elimination of the Taylor system in tests/test_oracle.py (test_weights_equal_taylor_solve).
 #include <stdexcept>
 #include <utility>
 #include <vector>

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SWB_LIB") or os.path.join(_HERE, "_lib", "libswb.so")  # SWB_LIB: development A/B
 
-SWB_OK, SWB_EINVAL, SWB_ECUDA, SWB_EUNSTABLE = 0, 1, 2, 3
+SWB_OK, SWB_EINVAL, SWB_ECUDA, SWB_EUNSTABLE, SWB_ERANGE = 0, 1, 2, 3, 4
 FORM_FACTORISED, FORM_PLAIN_F64, FORM_PLAIN_F32, FORM_FACTORISED_SIMPLE = 0, 1, 2, 3
 FORM_FACTORISED_SIMPLE_F32C = 4
 
@@ -26,7 +26,7 @@ class SwbProblem(C.Structure):
         ("n_receivers", C.c_int32), ("receivers", C.POINTER(C.c_int32)), ("form", C.c_int32),
         ("time_block", C.c_int32), ("device", C.c_int32), ("slab_lo", C.c_int32),
         ("slab_hi", C.c_int32), ("n_coord_receivers", C.c_int32),
-        ("coord_receivers", C.POINTER(C.c_double)),
+        ("coord_receivers", C.POINTER(C.c_double)), ("check_bounds", C.c_int32),
     ]
 
 
@@ -53,6 +53,7 @@ def _load() -> C.CDLL:
         "swb_create": (C.c_int, [P(SwbProblem), P(h)]),
         "swb_set_level": (C.c_int, [h, C.c_int, fp]),
         "swb_get_level": (C.c_int, [h, C.c_int, fp]),
+        "swb_get_level_padded": (C.c_int, [h, C.c_int, fp, C.c_int]),
         "swb_apply": (C.c_int, [h, C.c_int, C.c_int, fp, P(C.c_int32), fp]),
         "swb_apply_async": (C.c_int, [h, C.c_int, C.c_int]),
         "swb_apply_adjoint": (C.c_int, [h, C.c_int, fp, fp, fp, P(C.c_int32)]),
@@ -82,8 +83,8 @@ def _load() -> C.CDLL:
 
 lib = _load()
 
-# C-ABI entry points declared in include/swb.h (checked by tests/test_capi_symbols.py).
-EXPORTED = ["swb_create", "swb_set_level", "swb_get_level", "swb_apply", "swb_apply_async", "swb_apply_adjoint",
+# C-ABI entry points declared in include/swb.h (checked by tests/test_capi.py::test_header_symbols_exported).
+EXPORTED = ["swb_create", "swb_set_level", "swb_get_level", "swb_get_level_padded", "swb_apply", "swb_apply_async", "swb_apply_adjoint",
             "swb_apply_snapshots",
             "swb_collect", "swb_stream", "swb_get_stats", "swb_destroy", "swb_last_error",
             "swb_export_ghosts", "swb_link_neighbours", "swb_link_local", "swb_fd_weights",

@@ -5,6 +5,8 @@
 // the kernel-choice baseline for the TMA 2.5D kernel in k_tma.cu.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "k_common.cuh"
 #include "kernels.h"
 
@@ -248,11 +250,28 @@ __global__ void k_signal_flags(unsigned long long* lo_flag, unsigned long long* 
     __threadfence_system();
 }
 
+int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+        const int c = cache[dev].load(std::memory_order_relaxed);
+        if (c > 0) return c;
+    }
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = 1;
+    }
+    if (dev >= 0 && dev < 64) cache[dev].store(n, std::memory_order_relaxed);
+    return n;
+}
+
 cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
                             int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
                             int z_in1, unsigned* out, cudaStream_t s) {
     if (nx1 <= nx0) return cudaSuccess;
-    k_ring_max<<<148 * 8, 256, 0, s>>>(u, plane, P2, nx0, nx1, n1, n2, x_in0, x_in1, y_in0, y_in1,
+    k_ring_max<<<device_sm_count() * 8, 256, 0, s>>>(u, plane, P2, nx0, nx1, n1, n2, x_in0, x_in1, y_in0, y_in1,
                                        z_in0, z_in1, out);
     return cudaGetLastError();
 }

@@ -1181,7 +1181,7 @@ __global__ void k_damp_flags(const float* __restrict__ damp, long long plane, in
 }  // namespace
 
 cudaError_t tma_update_coefs(float* m, float* damp, long long n, float half_dt, cudaStream_t s) {
-    k_update_coefs<<<148 * 8, 256, 0, s>>>(m, damp, n, half_dt);
+    k_update_coefs<<<device_sm_count() * 8, 256, 0, s>>>(m, damp, n, half_dt);
     return cudaGetLastError();
 }
 

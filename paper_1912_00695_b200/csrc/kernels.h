@@ -14,6 +14,9 @@ struct TbCtl {
     int ctas;                 // CTAs per stage; the grid is 2 * ctas
 };
 
+// SMs of the current device (cached per device; grid sizing of the element-wise kernels).
+int device_sm_count();
+
 // One-thread-per-point stencil step; form: 0 factorised, 1 plain FP64, 2 plain FP32.
 cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ctl& c,
                           const Peer& p, cudaStream_t s);

@@ -445,6 +445,26 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         if (lo < 0 || hi > p->shape[0] || lo >= hi) return fail(SWB_EINVAL, "bad slab range");
         if (hi - lo < HU) return fail(SWB_EINVAL, "slab thinner than SO/2 planes");
     }
+    if (p->check_bounds && p->has_source) {
+        // RunOptions::check_bounds: the interpreter's first failing access.  The stencil cluster
+        // (update interior [H, n-1-H], offsets <= SO/2 into u padded by SO/2; m, damp at offset 0)
+        // never leaves the allocation; the source cluster runs after it (src/pipeline.cpp:89-113)
+        // and loads u+ then m at the point (its update u+ + dt^2 amp / m, then the store).
+        const char* dn3[3] = {"x", "y", "z"};
+        const int halo_u = HU, halo_m = 1;
+        for (int f = 0; f < 2; ++f) {
+            const int hf = f == 0 ? halo_u : halo_m;
+            for (int d = 0; d < 3; ++d)
+                if (p->source[d] + hf < 0 || p->source[d] + hf >= p->shape[d] + 2 * hf)
+                    return fail(SWB_ERANGE, std::string("access to ") + (f == 0 ? "u" : "m") +
+                                                " leaves the allocation in " + dn3[d] + " at step 0");
+        }
+    }
+    if (p->check_bounds)
+        for (int r = 0; r < p->n_receivers; ++r)  // receivers (an addition) sample u at offset 0
+            for (int d = 0; d < 3; ++d)
+                if (p->receivers[3 * r + d] + HU < 0 || p->receivers[3 * r + d] + HU >= p->shape[d] + 2 * HU)
+                    return fail(SWB_ERANGE, "receiver " + std::to_string(r) + " access to u leaves the allocation");
     if (p->has_source) {
         for (int d = 0; d < 3; ++d)
             if (p->source[d] < HU || p->source[d] > p->shape[d] - 1 - HU)
@@ -679,8 +699,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     mark("adjoint sampler");
     // Kernel choice: the TMA 2.5D kernel for the factorised form when the plan fits.
     if (h->form == SWB_FORM_FACTORISED) {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+        int sms = device_sm_count();  // (current device = h->device, set by setup_device)
         if (const char* cap = std::getenv("SWB_MAX_CTAS")) sms = std::max(1, std::min(sms, std::atoi(cap)));
         h->plan = tma_plan(HU, g, sms);
         if (h->plan.ok && h->K.iso) {
@@ -740,6 +759,24 @@ int swb_get_level(swb_handle* h, int level, float* dst) {
                                sizeof(float) * h->P2, row,
                                static_cast<size_t>(h->hi - h->lo) * h->n1, cudaMemcpyDeviceToHost,
                                h->stream));
+    SWB_CUDA(cudaStreamSynchronize(h->stream));
+    return SWB_OK;
+}
+
+int swb_get_level_padded(swb_handle* h, int level, float* dst, int halo) {
+    if (!h || !dst || level < 0 || level > 2 || halo < 0) return fail(SWB_EINVAL, "bad get_level_padded arguments");
+    if (h->pending) return fail(SWB_EINVAL, "an asynchronous apply is pending");
+    SWB_CUDA(cudaSetDevice(h->device));
+    // owned planes [lo, hi) of the level -> the padded host block at (lo + halo, halo, halo)
+    cudaMemcpy3DParms cp{};
+    cp.srcPtr = make_cudaPitchedPtr(h->u + level * h->level_floats + h->gb * h->plane, sizeof(float) * h->P2,
+                                    sizeof(float) * h->n2, h->n1);
+    cp.dstPtr = make_cudaPitchedPtr(dst, sizeof(float) * (h->n2 + 2 * halo), sizeof(float) * (h->n2 + 2 * halo),
+                                    h->n1 + 2 * halo);
+    cp.dstPos = make_cudaPos(sizeof(float) * halo, halo, h->lo + halo);
+    cp.extent = make_cudaExtent(sizeof(float) * h->n2, h->n1, h->hi - h->lo);
+    cp.kind = cudaMemcpyDeviceToHost;
+    SWB_CUDA(cudaMemcpy3DAsync(&cp, h->stream));
     SWB_CUDA(cudaStreamSynchronize(h->stream));
     return SWB_OK;
 }
@@ -1043,6 +1080,9 @@ int swb_destroy(swb_handle* h) {
     if (!h) return SWB_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    // snapshot copies may still read u (an apply_snapshots that returned early on an error)
+    if (h->s_d2d) cudaStreamSynchronize(h->s_d2d);
+    if (h->s_d2h) cudaStreamSynchronize(h->s_d2h);
     if (h->ipc_lo_u) cudaIpcCloseMemHandle(h->ipc_lo_u);
     if (h->ipc_hi_u) cudaIpcCloseMemHandle(h->ipc_hi_u);
     if (h->ipc_lo_f) cudaIpcCloseMemHandle(h->ipc_lo_f);
@@ -1058,8 +1098,6 @@ int swb_destroy(swb_handle* h) {
     for (void* q : {static_cast<void*>(h->d_adj), static_cast<void*>(h->d_src_trace),
                     static_cast<void*>(h->d_trace)})
         if (q) cudaFree(q);
-    if (h->s_d2h) cudaStreamSynchronize(h->s_d2h);
-    if (h->s_d2d) cudaStreamSynchronize(h->s_d2d);
     for (int j = 0; j < swb_handle::kSnapSlots; ++j) {
         if (h->d_stage[j]) cudaFree(h->d_stage[j]);
         if (h->ev_d2d[j]) cudaEventDestroy(h->ev_d2d[j]);

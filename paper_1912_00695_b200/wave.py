@@ -55,12 +55,18 @@ class InstabilityError(RuntimeError):
         return self._step
 
 
+class OutOfRangeError(IndexError):
+    """std::out_of_range of the interpreter's RunOptions::check_bounds (src/executor.cpp:417-428)."""
+
+
 def _check(rc: int, step: int = -1) -> None:
     if rc == N.SWB_OK:
         return
     msg = N.last_error()
     if rc == N.SWB_EINVAL:
         raise ValueError(msg)
+    if rc == N.SWB_ERANGE:
+        raise OutOfRangeError(msg)
     if rc == N.SWB_EUNSTABLE:
         raise InstabilityError(step, msg)
     raise N.CudaError(msg)
@@ -277,9 +283,11 @@ class Field:
 
 @dataclass
 class RunOptions:
-    """exec::RunOptions (include/stencilc/executor.hpp:72-79).  ``threads`` and
-    ``check_bounds`` are accepted for compatibility (all accesses are in-bounds by
-    construction of the device layout)."""
+    """exec::RunOptions (include/stencilc/executor.hpp:72-79).  ``threads`` is accepted for
+    compatibility (the device decides the parallelism).  ``check_bounds`` validates every access
+    of the operator against the reference's padded allocation before stepping and raises
+    OutOfRangeError (std::out_of_range) with the interpreter's message at the first one outside
+    (only a source point moved after make_wave_problem can get there)."""
     threads: int = 1
     check_bounds: bool = False
     initial_u: Optional[Sequence[np.ndarray]] = None
@@ -320,7 +328,8 @@ class Operator:
                  receiver_coords: Optional[np.ndarray] = None,
                  device: int = 0, time_block: int = 1,
                  slab: Optional[Tuple[int, int]] = None,
-                 m: Optional[np.ndarray] = None, damp: Optional[np.ndarray] = None):
+                 m: Optional[np.ndarray] = None, damp: Optional[np.ndarray] = None,
+                 check_bounds: bool = False):
         self.problem = problem
         self.form = form or form_for(dse)
         if self.form not in _FORMS:
@@ -374,6 +383,7 @@ class Operator:
             p.n_coord_receivers = rc.shape[0]
             p.coord_receivers = rc.ctypes.data_as(C.POINTER(C.c_double))
         p.form = _FORMS[self.form]
+        p.check_bounds = 1 if check_bounds else 0
         p.time_block = int(time_block)
         p.device = int(device)
         if slab is not None:
@@ -394,6 +404,10 @@ class Operator:
     def get_level(self, level: int, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.zeros(self.problem.shape, np.float32)
+        elif (not isinstance(out, np.ndarray) or out.dtype != np.float32
+              or out.size != self.problem.cell_count() or not out.flags.c_contiguous):
+            # the library writes a whole grid of float32 through this pointer
+            raise ValueError("out must be a grid-sized C-contiguous float32 array")
         _check(N.lib.swb_get_level(self._h, int(level), N.fptr(out)))
         return out
 
@@ -544,7 +558,7 @@ def run(problem: WaveProblem, options: Optional[RunOptions] = None,
     """
     options = options or RunOptions()
     op = Operator(problem, dse, form=form, receivers=receivers, receiver_coords=receiver_coords,
-                  device=device)
+                  device=device, check_bounds=options.check_bounds)
     try:
         if options.initial_u is not None:
             if len(options.initial_u) > 3:
@@ -566,7 +580,12 @@ def run(problem: WaveProblem, options: Optional[RunOptions] = None,
                 smax.append(r.step_max_abs[0])
                 if r.rec_traces is not None:
                     traces.append(r.rec_traces[0])
-                options.on_step(s, Field(problem, op.levels()), (s + 1) % 3)
+                # step s writes only level (s+1)%3: one level per step after the first download
+                if s == 0:
+                    lv = op.levels()
+                else:
+                    op.get_level((s + 1) % 3, lv[(s + 1) % 3])
+                options.on_step(s, Field(problem, lv), (s + 1) % 3)
             res = RunResult(Field(problem), np.array(smax, np.float32), wall, 0,
                             problem.steps % 3, np.array(traces) if traces else None)
         res.u = Field(problem, op.levels())

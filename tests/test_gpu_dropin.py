@@ -1,5 +1,5 @@
 """The reference tree rebuilt with integration/executor_b200.cpp instead of
-src/executor.cpp (oracle/_ref/dropin_run, built by `make -C oracle dropin` where
+src/executor.cpp (integration/_build/dropin_run, built by `make -C integration` where
 /root/reference exists): the reference's own call sequence
 make_wave_problem -> wave_equations -> lower -> optimize_all -> build_iet -> exec::run
 now runs on the B200 kernels.  basic IET: bit-exact with the oracle; aggressive IET:
@@ -14,7 +14,7 @@ from oracle import bindings as O
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-EXE = os.path.join(ROOT, "oracle", "_ref", "dropin_run")
+EXE = os.path.join(ROOT, "integration", "_build", "dropin_run")
 
 
 def run_dropin(dse, shape, so, steps, damp, tmp_path):
@@ -64,3 +64,22 @@ def test_reference_api_instability_error(dse, tmp_path):
         with pytest.raises(P.InstabilityError) as ei:
             P.run(P.make_wave_problem(cfg), dse=P.DseLevel.aggressive)
         assert step == ei.value.step()
+
+
+@pytest.mark.skipif(not os.path.exists(EXE), reason="drop-in binary not built (needs /root/reference)")
+@pytest.mark.parametrize("dse", ["basic", "aggressive"])
+def test_reference_api_on_step_and_check_bounds(dse, tmp_path):
+    """RunOptions::on_step through the drop-in: the callback's Field shows the newest level
+    (its max|u| is step_max_abs[step]) and the previous newest level unchanged, with one level
+    downloaded per step; check_bounds on the canonical tree passes and changes nothing."""
+    shape, so, steps = (20, 21, 22), 8, 9
+    env = dict(os.environ, DROPIN_ON_STEP="1", DROPIN_CHECK_BOUNDS="1")
+    out = tmp_path / "cb.bin"
+    p = subprocess.run([EXE, dse, *map(str, shape), str(so), str(steps), "0.05", str(out)],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert p.returncode == 0 and "on_step match -1" in p.stdout, p.stdout + p.stderr
+    plain = tmp_path / "plain.bin"
+    q = subprocess.run([EXE, dse, *map(str, shape), str(so), str(steps), "0.05", str(plain)],
+                       capture_output=True, text=True, timeout=120)
+    assert q.returncode == 0, q.stdout + q.stderr
+    assert out.read_bytes() == plain.read_bytes()
