@@ -18,7 +18,11 @@ NVLink peer memory (weak scaling).
   cpu_baseline  the reference's own exec::run (basic IET, all host threads) on a bounded
             sample of the same workload (rank 0, N=1)
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c4]
+
+--gpus N without torchrun re-launches itself under torch.distributed.run with N ranks (one per
+GPU); under torchrun WORLD_SIZE must equal N.  --workload c4 is BASELINE config 4: 512^3 global,
+SO 8, absorbing layer (damp_width 10, damp_max 2e-5), strong scaling over the N GPUs.
 """
 from __future__ import annotations
 
@@ -36,7 +40,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPts/s & % HBM roofline (3D acoustic, 256³, SO 4–16) at 1/2/4/8 B200 vs CPU"
-BYTES_PER_POINT = 20  # u[t], u[t-1], m, damp read + u[t+1] written, FP32
+BYTES_PER_POINT = 20  # u[t], u[t-1], m, damp read + u[t+1] written, FP32 (SURVEY §8(d) convention)
+# bytes the kernel must move per point: u[t], u[t-1], B = 1/(m+g) read + u[t+1] written; the A tile
+# (the damping coefficient) only where damp != 0, so 16 B/pt on an undamped grid
+BYTES_REQUIRED_UNDAMPED = 16
+DAMP_C4 = 3 * 1500.0 / (10 * 10.0) / 1500.0 ** 2  # config 4 layer: 3c/(width h) x m-scale ~ 2e-5
 FLOPS_AGGRESSIVE = {2: 24, 4: 34, 8: 57, 12: 75, 16: 93}  # reference's count_scalar_ops
 FLOPS_BASIC = {2: 69, 4: 105, 8: 165, 12: 225, 16: 285}
 
@@ -188,14 +196,22 @@ def allsum(x, world):
     return float(t.item())
 
 
-def traffic_from_profiles(so):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+def traffic_from_profiles(so, n=256):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the stencil kernel, from the
+    committed ncu capture: the steady-state one (a range of consecutive launches with
+    --cache-control none, so u[t+1] written back from L2 is counted) when present, else the
+    cold-cache per-launch capture.  Returns (bytes, kind)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d["k_tma"][f"so{so}"]["dram_bytes_per_launch"]
+        st = d.get("k_tma_steady", {}).get(f"n{n}_so{so}")
+        if st:
+            return st["dram_bytes_per_launch"], "steady-state (ncu range, --cache-control none)"
+        if n == 256:
+            return d["k_tma"][f"so{so}"]["dram_bytes_per_launch"], "cold-cache single launch (ncu)"
     except Exception:
-        return None
+        pass
+    return None, None
 
 
 def host_threads():
@@ -212,6 +228,36 @@ def pinned(shape):
     return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
 
 
+def link_report(op, rank, device):
+    """One line per rank on stderr: the slab, the neighbours' devices and how each halo exchange
+    is ordered (fused = inside the stencil kernel over peer memory)."""
+    st = op.stats()
+    lo, hi = op.slab
+    print(f"[rank {rank}] device {device} slab [{lo},{hi}) grid {st.grid} CTAs | "
+          f"lower: device {st.peer_lo} fused {st.fused_lo} | upper: device {st.peer_hi} fused {st.fused_hi}",
+          file=sys.stderr, flush=True)
+
+
+def measure_operator(P, D, prob, args, rank, world, device, slab, m, damp, steps, warm):
+    """Device-resident GPts/s of `prob` over this rank's slab (max over ranks)."""
+    o2 = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
+    if world > 1:
+        D.exchange_and_link(o2, rank, world)
+    o2.apply(warm, 0)
+    barrier(world)
+    o2.apply_async(steps, warm)
+    o2.collect(steps)
+    barrier(world)
+    t = allmax(o2.stats().device_ms * 1e-3, world)
+    lo, hi = o2.slab
+    so = prob.space_order
+    hh = so // 2
+    n0, n1, n2 = prob.shape
+    pl = (min(hi, n0 - hh) - max(lo, hh)) * (n1 - so) * (n2 - so)
+    o2.close()
+    return allsum(pl, world) * steps / t / 1e9, pl
+
+
 def run_ours(args, rank, world, local):
     import torch
 
@@ -221,12 +267,18 @@ def run_ours(args, rank, world, local):
     ndev = torch.cuda.device_count()
     if ndev == 0:
         raise SystemExit("no CUDA device")
+    if ndev < world and not args.allow_shared_gpu:
+        raise SystemExit(f"{world} ranks but only {ndev} visible GPU(s): one rank per GPU "
+                         f"(--allow-shared-gpu runs ranks on shared devices, for plumbing tests only)")
     device = local % ndev
     n, so, K, W = args.n, args.so, args.steps, args.warmup
-    shape = (n * world, n, n)
-    nt_total = K + W + 8
+    c4 = args.workload == "c4"
+    scaling = args.scaling or ("strong" if c4 else "weak")
+    shape = (n, n, n) if scaling == "strong" else (n * world, n, n)
+    damp_max = DAMP_C4 if c4 else 0.0
+    nt_total = max(K, 1000) + W + 8
     prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
-                                                   steps=nt_total))
+                                                   steps=nt_total, damp_max=damp_max, damp_width=10))
     slab = D.slab_bounds(shape[0], world, rank) if world > 1 else None
     m, damp = pinned(shape), pinned(shape)  # user-side host buffers in pinned memory
     m[...] = prob.m_data()
@@ -234,9 +286,10 @@ def run_ours(args, rank, world, local):
     op = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
     if world > 1:
         D.exchange_and_link(op, rank, world)
+        link_report(op, rank, device)
     lo, hi = op.slab
     h = so // 2
-    pts_local = (min(hi, n * world - h) - max(lo, h)) * (n - so) * (n - so)
+    pts_local = (min(hi, shape[0] - h) - max(lo, h)) * (n - so) * (n - so)
     pts_total = allsum(pts_local, world)
     # warm-up
     op.apply(W, 0)
@@ -260,43 +313,50 @@ def run_ours(args, rank, world, local):
     mean_launch_s = st.device_ms * 1e-3 / stencil_launches
     hbm, peak_kind = peaks()
     achieved = BYTES_PER_POINT * pts_local * (K / stencil_launches) / mean_launch_s / 1e9
+    req = BYTES_PER_POINT if damp_max > 0 else BYTES_REQUIRED_UNDAMPED
+    traffic, traffic_kind = traffic_from_profiles(so, n) if not c4 and world == 1 else (None, None)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": traffic_from_profiles(so),
+            "frac": round(achieved / hbm, 4), "traffic": traffic,
             "peak_kind": peak_kind, "kernel": "k_tma (factorised 2.5D TMA stencil)",
-            "bytes_per_point": BYTES_PER_POINT}
+            "bytes_per_point": BYTES_PER_POINT,
+            # the same launch time against the bytes this problem requires (16 B/pt undamped: no
+            # damping-coefficient tile is loaded) and against the DRAM bytes ncu measured
+            "bytes_per_point_required": req,
+            "frac_required": round(req * pts_local / mean_launch_s / 1e9 / hbm, 4),
+            "dram_frac": (round(traffic / mean_launch_s / 1e9 / hbm, 4) if traffic else None),
+            "traffic_kind": traffic_kind}
     # ---- sweep over the other space orders (device-resident, same protocol) ----
     sweep = {}
-    if not args.no_sweep:
+    if not args.no_sweep and not c4:
         for s2 in (4, 8, 12, 16):
             if s2 == so:
-                sweep[f"so{s2}"] = {"gpts": round(value, 2), "frac": roof["frac"],
-                                    "gflops": round(value * FLOPS_AGGRESSIVE[s2], 1),
-                                    "oi_flop_per_byte": round(FLOPS_AGGRESSIVE[s2] / BYTES_PER_POINT, 3)}
-                continue
-            p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
-                                                         space_order=s2, steps=args.sweep_steps + 16))
-            o2 = P.Operator(p2, form="factorised", device=device, slab=slab, m=m, damp=damp)
-            if world > 1:
-                D.exchange_and_link(o2, rank, world)
-            o2.apply(5, 0)
-            barrier(world)
-            torch.cuda.synchronize(device)
-            o2.apply_async(args.sweep_steps, 5)
-            o2.collect(args.sweep_steps)
-            barrier(world)
-            t2 = allmax(o2.stats().device_ms * 1e-3, world)
-            hh = s2 // 2
-            pl = (min(hi, n * world - hh) - max(lo, hh)) * (n - s2) * (n - s2)
-            g2 = allsum(pl, world) * args.sweep_steps / t2 / 1e9
+                g2 = value
+            else:
+                p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
+                                                             space_order=s2, steps=args.sweep_steps + 16))
+                g2, _ = measure_operator(P, D, p2, args, rank, world, device, slab, m, damp, args.sweep_steps, 5)
             sweep[f"so{s2}"] = {"gpts": round(g2, 2),
                                 "frac": round(BYTES_PER_POINT * g2 / world / hbm, 4),
+                                "frac_required": round(BYTES_REQUIRED_UNDAMPED * g2 / world / hbm, 4),
                                 "gflops": round(g2 * FLOPS_AGGRESSIVE[s2], 1),
                                 "oi_flop_per_byte": round(FLOPS_AGGRESSIVE[s2] / BYTES_PER_POINT, 3)}
-            o2.close()
+    # ---- BASELINE config 4 geometry on this node (512^3 global, SO 8, absorbing layer): the
+    # damped case, where the damping-coefficient tiles near the faces are loaded ----
+    damped = None
+    if not args.no_sweep and not c4:
+        p4 = P.make_wave_problem(P.WaveProblemConfig(shape=(512, 512, 512), spacing=(10.0, 10.0, 10.0),
+                                                     space_order=8, steps=args.sweep_steps + 16,
+                                                     damp_max=DAMP_C4, damp_width=10))
+        slab4 = D.slab_bounds(512, world, rank) if world > 1 else None
+        g4, _ = measure_operator(P, D, p4, args, rank, world, device, slab4, None, None, args.sweep_steps // 2, 5)
+        damped = {"workload": "BASELINE config 4: 512^3 global, SO 8, damp_width 10, damp_max %.3g, "
+                              "z-slabs over the N GPUs (strong scaling)" % DAMP_C4,
+                  "gpts": round(g4, 2), "frac": round(BYTES_PER_POINT * g4 / world / hbm, 4),
+                  "steps": args.sweep_steps // 2}
     # ---- K3 temporal blocking (two steps per launch) vs K1, same protocol (BASELINE config 5's
     # comparison; single domain -- linked slabs exchange halos every step and run K1) ----
     tblock = {}
-    if not args.no_sweep and world == 1:
+    if not args.no_sweep and world == 1 and not c4:
         for s2 in (4, 8, 12, 16):
             p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
                                                          space_order=s2, steps=args.sweep_steps + 16))
@@ -321,54 +381,95 @@ def run_ours(args, rank, world, local):
         for a in init:
             a[...] = 0.0
         out = [pinned(shape) for _ in range(3)]
-        runs = []
-        for _ in range(max(1, args.e2e_reps)):  # median of a few runs: host/PCIe timing varies run to run
-            barrier(world)
-            torch.cuda.synchronize(device)
-            t0 = time.perf_counter()
-            o3 = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
-            if world > 1:
-                D.exchange_and_link(o3, rank, world)
-            for l in range(3):
-                o3.set_level(l, init[l])
-            r = o3.apply(K, 0)
-            for l in range(3):
-                o3.get_level(l, out[l])
-            barrier(world)
-            t1 = time.perf_counter()
-            o3.close()
-            runs.append(allmax(t1 - t0, world))
-        e2e_s = float(np.median(runs))
-        planes = hi - lo
-        # m, the 3 levels (and damp only when the problem is damped: zero damp is not copied)
-        h2d = (1 + (1 if float(prob.damp_max) != 0.0 else 0) + 3) * planes * n * n * 4 + 4 * prob.source.wavelet.size
-        d2h = 3 * planes * n * n * 4 + 4 * K
-        e2e = {"value": round(pts_total * K / e2e_s / 1e9, 2), "unit": "GPts/s",
-               "h2d_bytes_per_step": int(allsum(h2d, world) / K),
-               "d2h_bytes_per_step": int(allsum(d2h, world) / K),
-               "seconds": round(e2e_s, 4),
-               "runs_seconds": [round(x, 4) for x in runs],
-               "includes": "handle create (H2D m, damp if damped, wavelet) + H2D 3 levels (pinned) + K steps + "
-                           "D2H 3 levels + per-step max|u|"}
+
+        def e2e_at(steps, reps):
+            runs = []
+            for _ in range(max(1, reps)):  # median of a few runs: host/PCIe timing varies run to run
+                barrier(world)
+                torch.cuda.synchronize(device)
+                t0 = time.perf_counter()
+                o3 = P.Operator(prob, form="factorised", device=device, slab=slab, m=m, damp=damp)
+                if world > 1:
+                    D.exchange_and_link(o3, rank, world)
+                for l in range(3):
+                    o3.set_level(l, init[l])
+                o3.apply(steps, 0)
+                for l in range(3):
+                    o3.get_level(l, out[l])
+                barrier(world)
+                t1 = time.perf_counter()
+                o3.close()
+                runs.append(allmax(t1 - t0, world))
+            e2e_s = float(np.median(runs))
+            planes = hi - lo
+            # m, the 3 levels (and damp only when the problem is damped: zero damp is not copied)
+            h2d = (1 + (1 if float(prob.damp_max) != 0.0 else 0) + 3) * planes * n * n * 4 + \
+                4 * prob.source.wavelet.size
+            d2h = 3 * planes * n * n * 4 + 4 * steps
+            return {"value": round(pts_total * steps / e2e_s / 1e9, 2), "unit": "GPts/s",
+                    "h2d_bytes_per_step": int(allsum(h2d, world) / steps),
+                    "d2h_bytes_per_step": int(allsum(d2h, world) / steps),
+                    "steps": steps, "seconds": round(e2e_s, 4), "runs_seconds": [round(x, 4) for x in runs]}
+
+        e2e = e2e_at(K, args.e2e_reps)
+        e2e["includes"] = ("handle create (H2D m, damp if damped, wavelet) + H2D 3 levels (pinned) + K steps + "
+                           "D2H 3 levels + per-step max|u|")
+        if K != 1000:
+            # the copies are a fixed cost per call: the same contract at the paper's 1000 steps
+            e2e["at_1000_steps"] = e2e_at(1000, 3)
+        if world == 1 and not c4:
+            e2e["dropin_exec_run"] = dropin_e2e(n, so, 1000)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not c4:
         cpu = cpu_baseline(n, so, args.cpu_steps)
     if rank == 0:
         res = {
             "metric": METRIC, "value": round(value, 2), "unit": "GPts/s", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": round(dev_s * 1e3 / K, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"3D acoustic isotropic FD, {n}^3 per GPU (global {shape[0]}x{n}x{n}), "
-                                   f"SO {so}, factorised form, c=1500 m/s, h=10 m, dt=cfl_dt, Ricker 10 Hz",
+            "scaling": scaling, "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": (f"3D acoustic isotropic FD, {n}^3 per GPU (global {shape[0]}x{n}x{n}), "
+                                    f"SO {so}, factorised form, c=1500 m/s, h=10 m, dt=cfl_dt, Ricker 10 Hz")
+                       if not c4 else
+                       (f"BASELINE config 4: 3D acoustic isotropic FD, {n}^3 global over {world} GPU(s), SO {so}, "
+                        f"absorbing layer damp_width 10, damp_max {DAMP_C4:.3g}, factorised form"),
                        "grid": list(shape), "space_order": so, "time_steps_timed": K,
                        "points_per_step": int(pts_total),
-                       "l2": "inputs larger than L2 (20 B/pt x 15.3M pts = 305 MB/step > 126 MB)",
+                       "l2": "inputs larger than L2 (%d B/pt x %.1fM pts = %d MB/step > 126 MB)"
+                             % (BYTES_PER_POINT, pts_total / 1e6, BYTES_PER_POINT * pts_total / 1e6),
                        "parallelism": f"z-slab x{world} (reference dim 0), peer-memory halo exchange"},
             "gflops": round(value * FLOPS_AGGRESSIVE[so], 1),
-            "roofline": roof, "sweep": sweep, "temporal_blocking": tblock, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clocks,
+            "roofline": roof, "sweep": sweep, "damped": damped, "temporal_blocking": tblock,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(res), flush=True)
+
+
+def dropin_e2e(n, so, steps):
+    """exec::run through the reference's own API with the drop-in executor
+    (integration/_build/dropin_run: the reference's host code + integration/executor_b200.cpp +
+    libswb.so): make_wave_problem -> ... -> build_iet(aggressive) -> exec::run, which returns all
+    three levels in the reference's padded Field (pageable std::vector storage).  Median of 3 calls
+    after one warm-up call in the same process."""
+    exe = os.path.join(ROOT, "integration", "_build", "dropin_run")
+    if not os.path.exists(exe):
+        return {"unavailable": "integration/_build/dropin_run not built (needs /root/reference at build time)"}
+    env = dict(os.environ, DROPIN_REPS="3")
+    try:
+        p = subprocess.run([exe, "aggressive", str(n), str(n), str(n), str(so), str(steps), "0", "-"],
+                           capture_output=True, text=True, timeout=600, env=env)
+        kv = dict(x.split("=", 1) for x in p.stdout.split() if "=" in x)
+        run_s, wall_s = float(kv["run"]), float(kv["wall"])
+    except Exception as e:  # pragma: no cover
+        return {"error": f"{e}"}
+    pts = (n - so) ** 3 * steps
+    cells = n ** 3
+    return {"value": round(pts / run_s / 1e9, 2), "unit": "GPts/s", "steps": steps, "seconds": round(run_s, 4),
+            "time_loop_seconds": round(wall_s, 4),
+            "h2d_bytes_per_step": int((1 + 1) * cells * 4 / steps),
+            "d2h_bytes_per_step": int((3 * cells * 4 + 4 * steps) / steps),
+            "includes": "exec::run(iet, problem, {}) as called by a reference user: IET classification, "
+                        "handle create (H2D m, damp, wavelet), the time loop, D2H of 3 levels straight into "
+                        "the padded Field, RunResult assembly"}
 
 
 def cpu_baseline(n, so, steps):
@@ -399,9 +500,12 @@ def run_reference(args, rank, world):
         return
     from oracle import bindings as O
     n, so = args.n, args.so
-    shape = (n * world, n, n)
-    steps = max(1, min(args.steps, args.ref_steps))
-    cfg = O.OracleConfig(shape=shape, space_order=so, steps=steps)
+    c4 = args.workload == "c4"
+    scaling = args.scaling or ("strong" if c4 else "weak")
+    shape = (n, n, n) if scaling == "strong" else (n * world, n, n)
+    steps = max(1, min(args.steps, args.ref_steps if not c4 else 1))
+    cfg = O.OracleConfig(shape=shape, space_order=so, steps=steps, damp_max=DAMP_C4 if c4 else 0.0,
+                         damp_width=10)
     use_ref = O.ref_available()
     fn = O.ref_run if use_ref else O.port_run
     cores = host_threads()
@@ -411,10 +515,11 @@ def run_reference(args, rank, world):
     res = {
         "metric": METRIC, "value": round(gp, 6), "unit": "GPts/s", "n_gpus": world, "steps": steps,
         "warmup": 0, "ms_per_step": round(r["wall_seconds"] * 1e3 / steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp64-compute/fp32-storage", "data": "synthetic",
+        "scaling": scaling, "vs_baseline": None, "dtype": "fp64-compute/fp32-storage", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": f"3D acoustic isotropic FD, global {shape[0]}x{n}x{n}, SO {so}, basic DSE "
-                               f"(exec::run, OpenMP)", "grid": list(shape), "space_order": so},
+                               f"(exec::run, OpenMP)" + (f", damp_width 10, damp_max {DAMP_C4:.3g}" if c4 else ""),
+                   "grid": list(shape), "space_order": so},
         "cpu_baseline": {"value": round(gp, 6), "unit": "GPts/s", "cores": cores, "kind": kind,
                          "sample": f"{steps} time steps of the full grid (bounded sample; the K requested "
                                    f"steps would take {args.steps * r['wall_seconds'] / steps:.0f} s)"},
@@ -438,9 +543,28 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-reps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2: 256^3 per GPU, SO 8 (weak scaling); c4: BASELINE config 4, 512^3 global, SO 8, "
+                         "damped (strong scaling)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"])
+    ap.add_argument("--allow-shared-gpu", action="store_true",
+                    help="allow more ranks than visible GPUs (plumbing tests on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("warmup must be >= 3")
+    if args.workload == "c4" and args.n == 256:
+        args.n = 512
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (the driver does this itself)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.run(cmd).returncode)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}: launch one rank per GPU")
     rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -116,6 +116,12 @@ typedef struct swb_stats {
     uint64_t kernel_launches;  /* launches of this library's kernels in the last apply     */
     int32_t kernel_variant;    /* internal id of the stencil kernel chosen                 */
     int32_t launch_steps;      /* time steps per stencil launch                            */
+    /* linked z-slabs: neighbour device ordinals in this process's enumeration (-1: none, -2: not
+     * visible to this process) and whether the halo exchange with
+     * each neighbour is ordered inside the stencil kernel (1) or by wait/signal kernels (0) */
+    int32_t peer_lo, peer_hi;
+    int32_t fused_lo, fused_hi;
+    int32_t grid;              /* persistent CTAs of the stencil launch (0: not the TMA kernel) */
 } swb_stats;
 
 /* Engine construction (src/executor.cpp:142-148, 383-403): validates the problem, allocates

@@ -33,7 +33,8 @@ class SwbProblem(C.Structure):
 class SwbStats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("point_updates", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("kernel_variant", C.c_int32),
-                ("launch_steps", C.c_int32)]
+                ("launch_steps", C.c_int32), ("peer_lo", C.c_int32), ("peer_hi", C.c_int32),
+                ("fused_lo", C.c_int32), ("fused_hi", C.c_int32), ("grid", C.c_int32)]
 
 
 class CudaError(RuntimeError):

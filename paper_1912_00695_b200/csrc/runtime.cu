@@ -109,6 +109,17 @@ bool same_device(int device, const unsigned char* uuid) {
     return std::memcmp(prop.uuid.bytes, uuid, 16) == 0;
 }
 
+// Ordinal (in this process's enumeration) of the device with this UUID, or -2 if not visible.
+int device_of_uuid(const unsigned char* uuid) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return -2;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && std::memcmp(prop.uuid.bytes, uuid, 16) == 0) return d;
+    }
+    return -2;
+}
+
 }  // namespace
 
 struct swb_handle {
@@ -170,6 +181,7 @@ struct swb_handle {
     // per side: 1 = fused in-kernel ordering (both ends run the TMA kernel), 0 = wait/signal kernels
     int fused_lo = 0, fused_hi = 0;
     int nb_grid_lo = 0, nb_grid_hi = 0;      // neighbours' CTAs per step (fused counters)
+    int peer_dev_lo = -1, peer_dev_hi = -1;  // neighbours' device ordinals (-2: another process's)
     void* ipc_lo_u = nullptr;
     void* ipc_hi_u = nullptr;
     void* ipc_lo_f = nullptr;
@@ -1072,6 +1084,11 @@ int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas) {
 
 int swb_get_stats(swb_handle* h, swb_stats* out) {
     if (!h || !out) return fail(SWB_EINVAL, "null argument");
+    h->stats.peer_lo = h->lo_remote ? h->peer_dev_lo : -1;
+    h->stats.peer_hi = h->hi_remote ? h->peer_dev_hi : -1;
+    h->stats.fused_lo = h->fused_lo;
+    h->stats.fused_hi = h->fused_hi;
+    h->stats.grid = h->use_tma ? h->plan.grid : 0;
     *out = h->stats;
     return SWB_OK;
 }
@@ -1150,6 +1167,8 @@ int swb_link_local(swb_handle* lower, swb_handle* upper) {
     const int fused = fused_capable(lower) && fused_capable(upper) &&
                       (!same_dev || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
     lower->fused_hi = upper->fused_lo = fused;
+    lower->peer_dev_hi = upper->device;
+    upper->peer_dev_lo = lower->device;
     lower->nb_grid_hi = upper->plan.grid;
     upper->nb_grid_lo = lower->plan.grid;
     lower->stats.launch_steps = upper->stats.launch_steps = 1;  // linked slabs step one at a time
@@ -1213,6 +1232,7 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         h->fused_lo = b.fused_capable && fused_capable(h) &&
                       (!same_device(h->device, b.uuid) || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
         h->nb_grid_lo = b.grid;
+        h->peer_dev_lo = device_of_uuid(b.uuid);
     }
     if (upper_blob && upper_len) {
         IpcBlob b;
@@ -1225,6 +1245,7 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         h->fused_hi = b.fused_capable && fused_capable(h) &&
                       (!same_device(h->device, b.uuid) || std::getenv("SWB_FUSED_SAME_DEVICE") != nullptr);
         h->nb_grid_hi = b.grid;
+        h->peer_dev_hi = device_of_uuid(b.uuid);
     }
     h->stats.launch_steps = 1;  // linked slabs step one at a time
     compute_peer_ranges(h);

@@ -27,3 +27,10 @@ def test_warmup_below_three_is_rejected():
     p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--n", "32", "--steps", "1",
                         "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=120)
     assert p.returncode != 0
+
+
+def test_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert p.returncode != 0 and "WORLD_SIZE" in (p.stderr + p.stdout)
