@@ -75,8 +75,8 @@ typedef struct swb_problem {
     float spacing[3];          /* float(Grid::spacing()[d]) — bound as float (src/executor.cpp:193-194) */
     int32_t space_order;       /* even, 2..24 (GridFunction u space_order)                 */
     float dt;                  /* WaveProblem::dt                                          */
-    const float* m;            /* grid-sized WaveProblem::m_data()                         */
-    const float* damp;         /* grid-sized WaveProblem::damp_data(); NULL = all zero     */
+    const float* m;            /* grid-sized WaveProblem::m_data(); NULL = from velocity (below) */
+    const float* damp;         /* grid-sized WaveProblem::damp_data(); NULL = from damp_max/width (below) */
     const float* weights;      /* space_order+1 floats float(c_k), k=-SO/2..SO/2, of
                                   fd_coefficients(2, SO) (src/executor.cpp:136-138); NULL = computed */
     int32_t has_source;        /* WaveProblem::source engaged                              */
@@ -106,6 +106,15 @@ typedef struct swb_problem {
      * allocation in x at step 0").  Without it, a source outside the update interior is
      * SWB_EINVAL. */
     int32_t check_bounds;
+    /* Model fields computed on the device instead of uploaded (the reference computes them on the
+     * host, src/wave_model.cpp:16-45; the device results are bit-identical):
+     *   m == NULL:    velocity (grid-sized) is uploaded and m = 1.0f/(c*c) per cell (m_data);
+     *   damp == NULL: damp_max > 0 and damp_width > 0 give the boundary taper
+     *                 damp_max * (1 - dist/damp_width) within damp_width cells of a face
+     *                 (damp_data); otherwise damp is zero. */
+    const float* velocity;
+    float damp_max;
+    int32_t damp_width;
 } swb_problem;
 
 typedef struct swb_handle swb_handle;

@@ -238,7 +238,20 @@ struct Handle {
     ~Handle() { swb_destroy(h); }
 };
 
+// SWB_DROPIN_PROFILE=1: phase timings of exec::run on stderr (development)
+struct Phases {
+    bool on = std::getenv("SWB_DROPIN_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "exec::run %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 RunResult execute(const WaveProblem& problem, const RunOptions& options, int form) {
+    Phases ph;
     const auto& g = *problem.grid;
     if (g.rank() != 3) throw std::invalid_argument("the B200 operator supports rank-3 grids");
     swb_problem sp{};
@@ -248,9 +261,16 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     }
     sp.space_order = problem.space_order;
     sp.dt = problem.dt;
-    const std::vector<float> m = problem.m_data(), damp = problem.damp_data();
-    sp.m = m.data();
-    sp.damp = damp.data();
+    // m_data() and damp_data() (src/wave_model.cpp:16-45) are computed by the device from the
+    // velocity and the taper parameters, bit-identically (swb.h): the host does not spend ~70 ms
+    // per 256^3 grid on them, and a damped problem uploads one grid (the velocity) instead of two
+    if (problem.velocity.size() != problem.cell_count())
+        throw std::invalid_argument("velocity field size does not match the grid");
+    sp.m = nullptr;
+    sp.velocity = problem.velocity.data();
+    sp.damp = nullptr;
+    sp.damp_max = problem.damp_max;
+    sp.damp_width = problem.damp_width;
     std::vector<float> w;  // float(c_k) as rounded_const does (src/executor.cpp:136-138)
     for (const auto& [off, r] : sym::fd_coefficients(2, problem.space_order))
         w.push_back(static_cast<float>(r.to_double()));
@@ -266,6 +286,7 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     sp.check_bounds = options.check_bounds ? 1 : 0;
     Handle h;
     check(swb_create(&sp, &h.h));
+    ph.mark("swb_create");
     if (options.initial_u) {
         if (options.initial_u->size() > 3) throw std::invalid_argument("more initial levels than storage levels");
         for (size_t l = 0; l < options.initial_u->size(); ++l) {
@@ -275,6 +296,7 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
         }
     }
     RunResult result{Field(problem.u)};
+    ph.mark("initial levels + Field alloc");
     // device level -> the Field's padded storage in place (one pitched copy; the padding keeps
     // its zeros, as the interpreter never writes it)
     auto fetch = [&](int l) { check(swb_get_level_padded(h.h, l, result.u.level_data(l), result.u.halo())); };
@@ -303,8 +325,10 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
         }
     }
     auto t1 = std::chrono::steady_clock::now();
+    ph.mark("time loop");
     if (!options.on_step)
         for (int l = 0; l < 3; ++l) fetch(l);
+    ph.mark("3 levels D2H into Field");
     result.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
     // point_updates as the interpreter counts them (src/executor.cpp:303-304, 585)
     const int halo = std::max(problem.space_order / 2, 1);
@@ -319,11 +343,14 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
 // check_bounds first: the interpreter would compile and start executing any tree and throw at its
 // first access outside the allocation, before anything could tell it is not the acoustic IET.
 int classify_checked(const pipeline::IetNodePtr& iet, const WaveProblem& p, const RunOptions& options) {
+    Phases ph;
     if (options.check_bounds) {
         std::vector<pipeline::Bounds> box;
         check_bounds(iet, box);
     }
-    return classify(iet, p);
+    const int form = classify(iet, p);
+    ph.mark("classify (iet_hash x2)");
+    return form;
 }
 
 }  // namespace

@@ -27,6 +27,7 @@ class SwbProblem(C.Structure):
         ("time_block", C.c_int32), ("device", C.c_int32), ("slab_lo", C.c_int32),
         ("slab_hi", C.c_int32), ("n_coord_receivers", C.c_int32),
         ("coord_receivers", C.POINTER(C.c_double)), ("check_bounds", C.c_int32),
+        ("velocity", C.POINTER(C.c_float)), ("damp_max", C.c_float), ("damp_width", C.c_int32),
     ]
 
 

@@ -267,6 +267,51 @@ int device_sm_count() {
     return n;
 }
 
+namespace {
+// m = 1.0f / (c * c) as IEEE FP32 (the reference's host expression has no contraction: a
+// product, then a division)
+__global__ void k_m_from_velocity(float* __restrict__ m, long long n, int P2, int n2) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        if (static_cast<int>(i % P2) >= n2) continue;  // row padding stays 0
+        const float c = m[i];
+        m[i] = __fdiv_rn(1.0f, __fmul_rn(c, c));
+    }
+}
+
+// damp_data: dist = cells to the nearest face (global coordinates), damp_max (1 - dist/width)
+// for dist < width, else 0 (src/wave_model.cpp:25-45)
+__global__ void k_damp_taper(float* __restrict__ damp, int nl0, int n1, int P2, int xg_off, int n0, int n2,
+                             float damp_max, int width) {
+    const long long n = static_cast<long long>(nl0) * n1 * P2;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int z = static_cast<int>(i % P2);
+        const int y = static_cast<int>((i / P2) % n1);
+        const int x = static_cast<int>(i / (static_cast<long long>(P2) * n1)) + xg_off;
+        float v = 0.0f;
+        if (z < n2) {
+            const int dist = min(min(min(x, n0 - 1 - x), min(y, n1 - 1 - y)), min(z, n2 - 1 - z));
+            if (dist < width)
+                v = __fmul_rn(damp_max, __fsub_rn(1.0f, __fdiv_rn(static_cast<float>(dist), static_cast<float>(width))));
+        }
+        damp[i] = v;
+    }
+}
+}  // namespace
+
+cudaError_t launch_m_from_velocity(float* m, long long n, int P2, int n2, cudaStream_t s) {
+    k_m_from_velocity<<<device_sm_count() * 8, 256, 0, s>>>(m, n, P2, n2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_damp_taper(float* damp, int nl0, int n1, int P2, int xg_off, int n0, int gn1, int n2,
+                              float damp_max, int width, cudaStream_t s) {
+    (void)gn1;
+    k_damp_taper<<<device_sm_count() * 8, 256, 0, s>>>(damp, nl0, n1, P2, xg_off, n0, n2, damp_max, width);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
                             int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
                             int z_in1, unsigned* out, cudaStream_t s) {

@@ -17,6 +17,14 @@ struct TbCtl {
 // SMs of the current device (cached per device; grid sizing of the element-wise kernels).
 int device_sm_count();
 
+// Model fields on the device (bit-identical to WaveProblem::m_data / damp_data,
+// src/wave_model.cpp:16-45): m <- 1.0f/(c*c) in place over a level-sized buffer holding the
+// velocity (row padding stays 0); damp <- the boundary taper for local planes [0, nl0) at global
+// plane offset xg_off of an n0 x n1 x n2 grid.
+cudaError_t launch_m_from_velocity(float* m, long long n, int P2, int n2, cudaStream_t s);
+cudaError_t launch_damp_taper(float* damp, int nl0, int n1, int P2, int xg_off, int n0, int gn1, int n2,
+                              float damp_max, int width, cudaStream_t s);
+
 // One-thread-per-point stencil step; form: 0 factorised, 1 plain FP64, 2 plain FP32.
 cudaError_t launch_simple(int H, int form, const Geo& g, const Coef& K, const Ctl& c,
                           const Peer& p, cudaStream_t s);

@@ -439,7 +439,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     if (p->space_order > 2 * kMaxH)
         return fail(SWB_EINVAL, "space_order above 24 is not supported");
     if (!(p->dt > 0.0f)) return fail(SWB_EINVAL, "dt must be positive");
-    if (!p->m) return fail(SWB_EINVAL, "m (squared slowness) is required");
+    if (!p->m && !p->velocity) return fail(SWB_EINVAL, "m (squared slowness) or the velocity is required");
     if (p->form < 0 || p->form > 4) return fail(SWB_EINVAL, "unknown stencil form");
     if (p->time_block < 0 || p->time_block > 2)
         return fail(SWB_EINVAL, "time_block must be 1 (one step per launch) or 2 (temporal blocking)");
@@ -554,18 +554,41 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     SWB_CUDA_C(cudaMemsetAsync(h->d_err, 0, sizeof(unsigned), h->stream));
 
     mark("malloc+memset");
-    // m / damp for every local plane (ghost planes included; they are never read).
+    // m / damp for every local plane (ghost planes included; they are never read).  Uploaded, or
+    // computed on the device from the velocity / the taper parameters (bit-identical to
+    // WaveProblem::m_data / damp_data, src/wave_model.cpp:16-45).
     const size_t row = sizeof(float) * h->n2;
-    const float* m_src = p->m + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
+    const float* m_src = (p->m ? p->m : p->velocity) + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
     SWB_CUDA_C(cudaMemcpy2DAsync(h->m, sizeof(float) * h->P2, m_src, row, row,
                                  static_cast<size_t>(h->nl0) * h->n1, cudaMemcpyHostToDevice,
                                  h->stream));
+    if (!p->m) SWB_CUDA_C(launch_m_from_velocity(h->m, h->level_floats, h->P2, h->n2, h->stream));
+    const bool damp_taper = !p->damp && p->damp_max > 0.0f && p->damp_width > 0;
     if (p->damp) {
         const float* d_src = p->damp + static_cast<size_t>(h->xg_off) * h->n1 * h->n2;
         SWB_CUDA_C(cudaMemcpy2DAsync(h->damp, sizeof(float) * h->P2, d_src, row, row,
                                      static_cast<size_t>(h->nl0) * h->n1, cudaMemcpyHostToDevice,
                                      h->stream));
+    } else if (damp_taper) {
+        SWB_CUDA_C(launch_damp_taper(h->damp, h->nl0, h->n1, h->P2, h->xg_off, h->n0, h->n1, h->n2, p->damp_max,
+                                     p->damp_width, h->stream));
     }
+    const bool has_damp = p->damp || damp_taper;
+    // host values of m / damp at single cells (source scaling, adjoint weights)
+    auto m_at = [&](size_t gi) -> float {
+        if (p->m) return p->m[gi];
+        const float c = p->velocity[gi];
+        return 1.0f / (c * c);
+    };
+    auto damp_at = [&](size_t gi) -> float {
+        if (p->damp) return p->damp[gi];
+        if (!damp_taper) return 0.0f;
+        const int x = static_cast<int>(gi / (static_cast<size_t>(h->n1) * h->n2));
+        const int y = static_cast<int>((gi / h->n2) % h->n1), z = static_cast<int>(gi % h->n2);
+        const int dist = std::min({x, h->n0 - 1 - x, y, h->n1 - 1 - y, z, h->n2 - 1 - z});
+        if (dist >= p->damp_width) return 0.0f;
+        return p->damp_max * (1.0f - static_cast<float>(dist) / static_cast<float>(p->damp_width));
+    };
     // FD weights: float(c_k) as the interpreter rounds them (src/executor.cpp:136-138).
     std::vector<float> w(static_cast<size_t>(2 * HU + 1));
     if (p->weights) {
@@ -610,7 +633,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             c.src_x = p->source[0] - h->xg_off;
             c.src_y = p->source[1];
             c.src_z = p->source[2];
-            c.src_m = p->m[(static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2]];
+            c.src_m = m_at((static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2]);
         }
     }
     c.wavelet = h->d_wavelet;
@@ -681,7 +704,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             if (lx < Hh || lx > h->n0 - 1 - Hh || y < Hh || y > h->n1 - 1 - Hh || z < Hh || z > h->n2 - 1 - Hh)
                 continue;
             const size_t gi = (static_cast<size_t>(lx) * h->n1 + y) * h->n2 + z;
-            const double mm = p->m[gi], dd = p->damp ? p->damp[gi] : 0.0;
+            const double mm = m_at(gi), dd = damp_at(gi);
             iw[q] = rw[q] / (mm + 0.5 * dd * dtd);
         }
         SWB_CUDA_C(hbuf_alloc(h, &h->d_inj_w, sizeof(double) * iw.size()));
@@ -698,7 +721,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     // Adjoint output sampler at the source point (owned slab only).
     if (c.has_src) {
         const size_t gi = (static_cast<size_t>(p->source[0]) * h->n1 + p->source[1]) * h->n2 + p->source[2];
-        const double mm = p->m[gi], dd = p->damp ? p->damp[gi] : 0.0, dtd = static_cast<double>(p->dt);
+        const double mm = m_at(gi), dd = damp_at(gi), dtd = static_cast<double>(p->dt);
         std::vector<long long> si(8, -1);
         std::vector<double> sw(8, 0.0);
         si[0] = local_index(p->source[0], p->source[1], p->source[2]);
@@ -719,7 +742,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             const size_t nflags = static_cast<size_t>(h->plan.columns) * std::max(0, g.x1 - g.x0);
             SWB_CUDA_C(hbuf_alloc(h, &h->d_dflag, std::max<size_t>(nflags, 1)));
             SWB_CUDA_C(cudaMemsetAsync(h->d_dflag, 0, std::max<size_t>(nflags, 1), h->stream));
-            if (p->damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
+            if (has_damp) SWB_CUDA_C(tma_damp_flags_device(h->plan, g, h->d_dflag, h->stream));
             h->plan.dflag = h->d_dflag;
             h->use_tma = true;
             // K1 reads m and damp only as the update coefficients B = 1/(m+g), A = (m-g)/(m+g):

@@ -342,19 +342,31 @@ class Operator:
         p.space_order = problem.space_order
         p.dt = float(problem.dt)
         # m / damp may be passed precomputed (e.g. pinned host buffers); they must equal
-        # problem.m_data() / problem.damp_data().
-        m = np.ascontiguousarray(problem.m_data() if m is None else m, np.float32)
-        if m.size != problem.cell_count():
-            raise ValueError("m size does not match the grid")
+        # problem.m_data() / problem.damp_data().  Otherwise the device computes them from the
+        # velocity and the taper parameters (bit-identical; swb.h swb_problem.velocity).
         w = rounded_weights(problem.space_order)
-        self._keep += [m, w]
-        p.m = N.fptr(m)
-        if float(problem.damp_max) == 0.0:
-            # damp_data() is identically zero (src/wave_model.cpp:25-45 scales by damp_max):
-            # NULL tells the library so -- it zero-fills in HBM instead of copying zeros over PCIe
+        self._keep.append(w)
+        if m is None:
+            vel = np.ascontiguousarray(problem.velocity, np.float32)
+            if vel.size != problem.cell_count():
+                raise ValueError("velocity size does not match the grid")
+            self._keep.append(vel)
+            p.m = N.fptr(None)
+            p.velocity = N.fptr(vel)
+        else:
+            m = np.ascontiguousarray(m, np.float32)
+            if m.size != problem.cell_count():
+                raise ValueError("m size does not match the grid")
+            self._keep.append(m)
+            p.m = N.fptr(m)
+        p.damp_max = float(problem.damp_max)
+        p.damp_width = int(problem.damp_width)
+        if damp is None or float(problem.damp_max) == 0.0:
+            # NULL: the taper on the device (zero without a layer, src/wave_model.cpp:29) --
+            # nothing crosses PCIe for it
             p.damp = N.fptr(None)
         else:
-            damp = np.ascontiguousarray(problem.damp_data() if damp is None else damp, np.float32)
+            damp = np.ascontiguousarray(damp, np.float32)
             if damp.size != problem.cell_count():
                 raise ValueError("damp size does not match the grid")
             self._keep.append(damp)

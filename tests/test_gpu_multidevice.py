@@ -55,16 +55,9 @@ def test_two_device_slabs_bitwise(so):
     for op in (a, b):
         for l in range(3):
             op.set_level(l, init[l])
-    import threading
-    res = {}
-
-    def go(name, op):
-        res[name] = op.apply(nt, 0)
-    ts = [threading.Thread(target=go, args=(k, o)) for k, o in (("a", a), ("b", b))]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
+    a.apply_async(nt, 0)
+    b.apply_async(nt, 0)
+    sma, smb = a.collect(nt), b.collect(nt)
     assert a.stats().kernel_launches == nt and b.stats().kernel_launches == nt  # no ordering kernels
     got = np.zeros_like(ref)
     for l in range(3):
@@ -72,8 +65,7 @@ def test_two_device_slabs_bitwise(so):
         got[l, :50] = la[:50]
         got[l, 50:] = lb[50:]
     assert np.array_equal(got, ref)
-    smax = np.maximum(res["a"].step_max_abs, res["b"].step_max_abs)
-    assert np.array_equal(smax, r1.step_max_abs)
+    assert np.array_equal(np.maximum(sma, smb), r1.step_max_abs)
     a.close()
     b.close()
 
