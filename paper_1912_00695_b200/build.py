@@ -42,31 +42,43 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libswb.so; with `variant`, a development build with extra -D `defines` into
+    _lib/variants/libswb_<variant>.so (loaded with SWB_LIB for A/B measurements)."""
+    out, obj_dir = OUT, OBJ
+    if variant:
+        out = os.path.join(HERE, "_lib", "variants", f"libswb_{variant}.so")
+        obj_dir = os.path.join(HERE, "_lib", "obj_" + variant)
+    elif not force and up_to_date():
         return OUT
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
     # one nvcc per translation unit, in parallel (the kernel TUs dominate), then one link
     from concurrent.futures import ThreadPoolExecutor
     objs = []
     cmds = []
     for src in sources():
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmds.append([nvcc()] + NVCC_FLAGS + ["-c", "-o", obj, src])
+        cmds.append([nvcc()] + flags + ["-c", "-o", obj, src])
     with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
         for cmd in cmds:
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
         list(ex.map(lambda c: subprocess.run(c, check=True, cwd=ROOT), cmds))
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True, cwd=ROOT)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python build.py [--force] [--variant NAME -DFOO=1 ...]
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else ""
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv, verbose=not var, variant=var, defines=defs))

@@ -256,8 +256,12 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     for (int i = 0; i < R1; ++i) {
         upv[i] = *reinterpret_cast<const float4*>(aux + i * kT2);
         bv[i] = *reinterpret_cast<const float4*>(aux + C::ATILE / 4 + i * kT2);
+#if SWB_COMBINE == 2
+        av[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + i * kT2) : bv[i];
+#else
         av[i] = has_damp ? *reinterpret_cast<const float4*>(aux + C::ATILE / 2 + i * kT2)
                          : make_float4(1.f, 1.f, 1.f, 1.f);
+#endif
     }
     mbar_arrive(empty_a + 8 * sa);
     mbar_arrive(empty_u + 8 * sp);  // plane p is no longer needed
@@ -1153,11 +1157,16 @@ __global__ void k_update_coefs(float* __restrict__ m, float* __restrict__ damp, 
         const float mf = m[i];
         const float g = damp[i] * half_dt;  // fl(damp dt/2), as the update has always rounded it
         float b = 0.f, a = 0.f;
+#if SWB_COMBINE == 2
+        b = mf + g;  // D
+        a = mf - g;  // E
+#else
         if (mf != 0.f) {
             const double mp = static_cast<double>(mf) + static_cast<double>(g);
             b = static_cast<float>(1.0 / mp);
             a = static_cast<float>((static_cast<double>(mf) - static_cast<double>(g)) / mp);
         }
+#endif
         m[i] = b;
         damp[i] = a;
     }

@@ -132,8 +132,19 @@ __device__ __forceinline__ float2 div2(float2 n, float2 d) {
 // The time update with the per-point coefficient fields of K1 (tma_update_coefs):
 //   u+ = u + A (u - u-) + B Lk,   A = (m - g)/(m + g),  B = 1/(m + g),  g = damp dt/2,
 // which is u + [(m - g)(u - u-) + Lk]/(m + g) without a division; A = 1 where no damping.
+#ifndef SWB_COMBINE
+#define SWB_COMBINE 0
+#endif
 __device__ __forceinline__ float2 update2(float2 u, float2 um, float2 Lk, float2 a, float2 b) {
+#if SWB_COMBINE == 0
     return fma2(b, Lk, fma2(a, sub2(u, um), u));
+#elif SWB_COMBINE == 1
+    // increment first, one rounding at the scale of u
+    return add2(u, fma2(b, Lk, mul2(a, sub2(u, um))));
+#else
+    // fields D = m + g (slot b), E = m - g (slot a): u+ = u + (E (u - u-) + Lk) / D
+    return add2(u, div2(fma2(a, sub2(u, um), Lk), b));
+#endif
 }
 
 // Advance a ring position (stage, phase) by one.
