@@ -25,11 +25,15 @@
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
+#include <future>
 #include <fstream>
 #include <limits>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "stencilc/executor.hpp"
 #include "swb.h"
@@ -47,7 +51,19 @@ Field::Field(sym::FunctionPtr fn)
     for (int d = static_cast<int>(padded_.size()) - 2; d >= 0; --d)
         strides_[d] = strides_[d + 1] * static_cast<std::size_t>(padded_[d + 1]);
     cells_ = strides_[0] * static_cast<std::size_t>(padded_[0]);
-    data_.assign(cells_ * static_cast<std::size_t>(levels_), 0.0f);
+    // zero-filled like the reference's data_.assign(n, 0.0f); the storage is reserved first and
+    // advised for transparent huge pages, so the first touch of a large field faults 2 MB pages
+    // instead of 4 KB ones (a 256^3 u field is 220 MB)
+    const std::size_t n = cells_ * static_cast<std::size_t>(levels_);
+    data_.reserve(n);
+#ifdef MADV_HUGEPAGE
+    if (n * sizeof(float) >= (std::size_t{8} << 20)) {
+        const std::uintptr_t a = (reinterpret_cast<std::uintptr_t>(data_.data()) + 4095) & ~std::uintptr_t{4095};
+        const std::uintptr_t b = (reinterpret_cast<std::uintptr_t>(data_.data() + n)) & ~std::uintptr_t{4095};
+        if (b > a) madvise(reinterpret_cast<void*>(a), b - a, MADV_HUGEPAGE);
+    }
+#endif
+    data_.resize(n, 0.0f);
 }
 
 std::size_t Field::cell_index(std::span<const int> point) const {
@@ -284,6 +300,10 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     sp.form = form;
     sp.time_block = 1;
     sp.check_bounds = options.check_bounds ? 1 : 0;
+    // The result Field (three zero-filled padded levels: 220 MB at 256^3) is built on another host
+    // thread while the device sets up and steps; without on_step nothing reads it before the end.
+    std::future<Field> field_later;
+    if (!options.on_step) field_later = std::async(std::launch::async, [&problem] { return Field(problem.u); });
     Handle h;
     check(swb_create(&sp, &h.h));
     ph.mark("swb_create");
@@ -295,17 +315,17 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
             check(swb_set_level(h.h, static_cast<int>(l), (*options.initial_u)[l].data()));
         }
     }
-    RunResult result{Field(problem.u)};
-    ph.mark("initial levels + Field alloc");
+    ph.mark("initial levels");
     // device level -> the Field's padded storage in place (one pitched copy; the padding keeps
     // its zeros, as the interpreter never writes it)
-    auto fetch = [&](int l) { check(swb_get_level_padded(h.h, l, result.u.level_data(l), result.u.halo())); };
+    auto fetch = [&](Field& f, int l) { check(swb_get_level_padded(h.h, l, f.level_data(l), f.halo())); };
     const int nt = problem.steps;
-    result.step_max_abs.assign(static_cast<size_t>(nt), 0.0f);
+    std::vector<float> smax(static_cast<size_t>(nt), 0.0f);
     int32_t bad = -1;
+    std::optional<Field> stepped;  // the on_step path's Field (the callbacks see it while stepping)
     auto t0 = std::chrono::steady_clock::now();
     if (!options.on_step) {
-        int rc = swb_apply(h.h, 0, nt, result.step_max_abs.data(), &bad, nullptr);
+        int rc = swb_apply(h.h, 0, nt, smax.data(), &bad, nullptr);
         if (rc == SWB_EUNSTABLE)
             throw InstabilityError(bad, "non-finite wave field at step " + std::to_string(bad) +
                                             " (unstable dt?)");
@@ -313,22 +333,26 @@ RunResult execute(const WaveProblem& problem, const RunOptions& options, int for
     } else {
         // on_step needs the host field after every step: one step per call (slow path).  Step s
         // writes only level (s+1)%3, so after one full download only the newest level moves.
-        for (int l = 0; l < 3; ++l) fetch(l);
+        stepped.emplace(problem.u);
+        for (int l = 0; l < 3; ++l) fetch(*stepped, l);
         for (int s = 0; s < nt; ++s) {
-            int rc = swb_apply(h.h, s, 1, &result.step_max_abs[static_cast<size_t>(s)], &bad, nullptr);
+            int rc = swb_apply(h.h, s, 1, &smax[static_cast<size_t>(s)], &bad, nullptr);
             if (rc == SWB_EUNSTABLE)
                 throw InstabilityError(bad, "non-finite wave field at step " + std::to_string(bad) +
                                                 " (unstable dt?)");
             check(rc);
-            fetch((s + 1) % 3);
-            options.on_step(s, result.u, (s + 1) % 3);
+            fetch(*stepped, (s + 1) % 3);
+            options.on_step(s, *stepped, (s + 1) % 3);
         }
     }
     auto t1 = std::chrono::steady_clock::now();
     ph.mark("time loop");
+    RunResult result{stepped ? std::move(*stepped) : field_later.get()};
+    ph.mark("Field ready (built during the steps)");
     if (!options.on_step)
-        for (int l = 0; l < 3; ++l) fetch(l);
+        for (int l = 0; l < 3; ++l) fetch(result.u, l);
     ph.mark("3 levels D2H into Field");
+    result.step_max_abs = std::move(smax);
     result.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
     // point_updates as the interpreter counts them (src/executor.cpp:303-304, 585)
     const int halo = std::max(problem.space_order / 2, 1);

@@ -43,6 +43,9 @@ using namespace tma;
 #ifndef SWB_UNROLL_MAXH
 #define SWB_UNROLL_MAXH 4  // rotate the register queue by renaming up to this halo (measured: +1 % at SO 8; I-cache misses beyond)
 #endif
+#ifndef SWB_LAP
+#define SWB_LAP 0  // development: Laplacian summation variants (probe_combine.py)
+#endif
 #ifndef SWB_TB_LEAD
 #define SWB_TB_LEAD 4
 #endif
@@ -203,6 +206,9 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
         float w[4 + 2 * C::A];
         load_window<H, C::A>(rowc, w);
         float2 al = splat(0.f), ah = splat(0.f);
+#if SWB_LAP == 2
+        const float2 cl = lo2(Q[i][UC]), chh = hi2(Q[i][UC]);
+#endif
 #pragma unroll
         for (int k = H; k >= 2; --k) {
             const float2 ck = splat(K.c[k]);
@@ -210,6 +216,17 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
             const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2);
             const float4& xm = Q[i][(UC + NQ - k) % NQ];
             const float4& xp = Q[i][(UC + k) % NQ];
+#if SWB_LAP == 2
+            // full difference form: every neighbour minus the centre first
+            const float2 zl = make_float2((w[C::A - k] - cl.x) + (w[C::A + k] - cl.x),
+                                          (w[C::A + 1 - k] - cl.y) + (w[C::A + 1 + k] - cl.y));
+            const float2 zh = make_float2((w[C::A + 2 - k] - chh.x) + (w[C::A + 2 + k] - chh.x),
+                                          (w[C::A + 3 - k] - chh.y) + (w[C::A + 3 + k] - chh.y));
+            const float2 sl = add2(add2(sub2(lo2(xm), cl), sub2(lo2(xp), cl)),
+                                   add2(add2(sub2(lo2(ym), cl), sub2(lo2(yp), cl)), zl));
+            const float2 sh = add2(add2(sub2(hi2(xm), chh), sub2(hi2(xp), chh)),
+                                   add2(add2(sub2(hi2(ym), chh), sub2(hi2(yp), chh)), zh));
+#else
             float2 zl, zh;
             if ((k & 1) == 0) {  // register-pair aligned: packed adds
                 zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]), make_float2(w[C::A + k], w[C::A + 1 + k]));
@@ -219,8 +236,15 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
                 zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
                 zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k], w[C::A + 3 - k] + w[C::A + 3 + k]);
             }
+#if SWB_LAP == 1
+            // per-axis grouping (pairs of one axis first, as the one-thread-per-point kernels)
+            const float2 sl = add2(add2(add2(lo2(xm), lo2(xp)), add2(lo2(ym), lo2(yp))), zl);
+            const float2 sh = add2(add2(add2(hi2(xm), hi2(xp)), add2(hi2(ym), hi2(yp))), zh);
+#else
             const float2 sl = add2(add2(lo2(xm), lo2(xp)), add2(add2(lo2(ym), lo2(yp)), zl));
             const float2 sh = add2(add2(hi2(xm), hi2(xp)), add2(add2(hi2(ym), hi2(yp)), zh));
+#endif
+#endif
             al = fma2(ck, sl, al);
             ah = fma2(ck, sh, ah);
         }
@@ -268,7 +292,11 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     ring_next<SA>(sa, pa_);
     if (++sp == SU) sp = 0;
     // ---- combine: u+ = u + A (u - u-) + B Lr (dt/h)^2 (coefficient fields, tma_update_coefs) ----
+#if SWB_LAP == 2
+    const float2 R3 = splat(K.R3f), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+#else
     const float2 R3 = splat(K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+#endif
     float4 out[R1];
 #pragma unroll
     for (int i = 0; i < R1; ++i) {

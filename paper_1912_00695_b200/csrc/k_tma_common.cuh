@@ -176,6 +176,9 @@ __device__ __forceinline__ unsigned zmask_of(int zc, int z0, int z1) {
     return m;
 }
 
+#ifndef SWB_PRED_EVICT_LAST
+#define SWB_PRED_EVICT_LAST 0
+#endif
 // Store one output float4 row and fold it into the max|u| bits.  Full lanes take one
 // STG.128; boundary lanes predicated scalar stores; no per-element branches (the partial
 // case only exists on the first/last z tile).
@@ -210,7 +213,13 @@ __device__ __forceinline__ void store_row_pred(float* dst, const float4& o, unsi
         "setp.eq.u32 pf, %0, 15;\n\t"
         "setp.eq.u32 pl, %0, 3;\n\t"
         "setp.eq.u32 ph, %0, 12;\n\t"
+#if SWB_PRED_EVICT_LAST
+        ".reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "@pf st.global.L2::cache_hint.v4.f32 [%1], {%2, %3, %4, %5}, pol;\n\t"
+#else
         "@pf st.global.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
+#endif
         "@pl st.global.v2.f32 [%1], {%2, %3};\n\t"
         "@ph st.global.v2.f32 [%1+8], {%4, %5};\n\t"
         "}" ::"r"(zmask), "l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)

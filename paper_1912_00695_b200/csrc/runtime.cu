@@ -222,6 +222,20 @@ int setup_device(int device) {
         checked.fetch_or(bit);
     }
     SWB_CUDA(cudaSetDevice(device));
+    // L2 set-aside for persisting (evict_last) lines: the stencil stores u[t+1] with an evict_last
+    // policy so that the next step's u[t] reads hit L2.  SWB_L2_PERSIST=<MB> (0 = off) overrides
+    // (development).
+    static std::atomic<unsigned long long> l2set{0};
+    if (!(l2set.load() & bit)) {
+        int maxp = 0;
+        if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0) {
+            size_t want = static_cast<size_t>(maxp);
+            if (const char* e = std::getenv("SWB_L2_PERSIST")) want = std::min(want, static_cast<size_t>(std::atoll(e)) << 20);
+            else want = 0;
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) cudaGetLastError();
+        }
+        l2set.fetch_or(bit);
+    }
     return SWB_OK;
 }
 
@@ -266,6 +280,11 @@ void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
     K.inject = dt * dt;
     K.iso = (p->spacing[0] == p->spacing[1] && p->spacing[1] == p->spacing[2]) ? 1 : 0;
     K.R3 = static_cast<float>(3.0 * K.R_d);
+    {
+        double r = c0;
+        for (int k = 1; k <= H; ++k) r += 2.0 * static_cast<double>(K.c[k]);
+        K.R3f = static_cast<float>(3.0 * r);
+    }
     const double h0 = static_cast<double>(p->spacing[0]);
     const double kap = (dt / h0) * (dt / h0);
     K.kap_hi = static_cast<float>(kap);
