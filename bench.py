@@ -353,26 +353,6 @@ def run_ours(args, rank, world, local):
                               "z-slabs over the N GPUs (strong scaling)" % DAMP_C4,
                   "gpts": round(g4, 2), "frac": round(BYTES_PER_POINT * g4 / world / hbm, 4),
                   "steps": args.sweep_steps // 2}
-    # ---- K3 temporal blocking (two steps per launch) vs K1, same protocol (BASELINE config 5's
-    # comparison; single domain -- linked slabs exchange halos every step and run K1) ----
-    tblock = {}
-    if not args.no_sweep and world == 1 and not c4:
-        for s2 in (4, 8, 12, 16):
-            p2 = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
-                                                         space_order=s2, steps=args.sweep_steps + 16))
-            o2 = P.Operator(p2, form="factorised", device=device, m=m, damp=damp, time_block=2)
-            o2.apply(6, 0)
-            torch.cuda.synchronize(device)
-            o2.apply_async(args.sweep_steps, 6)
-            o2.collect(args.sweep_steps)
-            st2 = o2.stats()
-            pl = (n - s2) ** 3
-            g2 = pl * args.sweep_steps / (st2.device_ms * 1e-3) / 1e9
-            k1 = sweep.get(f"so{s2}", {}).get("gpts")
-            tblock[f"so{s2}"] = {"gpts": round(g2, 2), "steps_per_launch": int(st2.launch_steps),
-                                 "frac": round(BYTES_PER_POINT * g2 / hbm, 4),
-                                 "vs_k1": round(g2 / k1, 3) if k1 else None}
-            o2.close()
     op.close()
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -438,7 +418,7 @@ def run_ours(args, rank, world, local):
                              % (BYTES_PER_POINT, pts_total / 1e6, BYTES_PER_POINT * pts_total / 1e6),
                        "parallelism": f"z-slab x{world} (reference dim 0), peer-memory halo exchange"},
             "gflops": round(value * FLOPS_AGGRESSIVE[so], 1),
-            "roofline": roof, "sweep": sweep, "damped": damped, "temporal_blocking": tblock,
+            "roofline": roof, "sweep": sweep, "damped": damped,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(res), flush=True)

@@ -86,7 +86,9 @@ typedef struct swb_problem {
     int32_t n_receivers;       /* on-grid receivers (new; the reference samples via on_step) */
     const int32_t* receivers;  /* [n_receivers][3] grid coordinates                        */
     int32_t form;              /* enum swb_form                                            */
-    int32_t time_block;        /* 1 = one launch per step; k>1 = temporal blocking of k steps */
+    int32_t time_block;        /* 1 (or 0): one launch per step.  The temporal-blocking kernel
+                                  (2 steps per launch) was measured 0.53-0.74x of the single-step
+                                  kernel on B200 and is retired; other values are SWB_EINVAL. */
     int32_t device;            /* CUDA device ordinal                                      */
     /* z-slab (reference dim 0) decomposition: this handle updates planes [slab_lo, slab_hi)
      * of the global grid; slab_hi <= 0 means the whole grid.  See swb_link_neighbours. */
@@ -124,7 +126,7 @@ typedef struct swb_stats {
     uint64_t point_updates;    /* RunResult::point_updates accumulated by this handle      */
     uint64_t kernel_launches;  /* launches of this library's kernels in the last apply     */
     int32_t kernel_variant;    /* internal id of the stencil kernel chosen                 */
-    int32_t launch_steps;      /* time steps per stencil launch                            */
+    int32_t launch_steps;      /* time steps per stencil launch (1)                        */
     /* linked z-slabs: neighbour device ordinals in this process's enumeration (-1: none, -2: not
      * visible to this process) and whether the halo exchange with
      * each neighbour is ordered inside the stencil kernel (1) or by wait/signal kernels (0) */

@@ -1,4 +1,4 @@
-// Shared device helpers of the TMA stencil kernels (k_tma.cu, k_sq.cu): mbarrier/TMA PTX
+// Device helpers of the TMA stencil kernel (k_tma.cu): mbarrier/TMA PTX
 // wrappers, packed FP32x2 arithmetic, tensor-map bundle, work schedule.
 #pragma once
 #include <cuda.h>
@@ -132,19 +132,10 @@ __device__ __forceinline__ float2 div2(float2 n, float2 d) {
 // The time update with the per-point coefficient fields of K1 (tma_update_coefs):
 //   u+ = u + A (u - u-) + B Lk,   A = (m - g)/(m + g),  B = 1/(m + g),  g = damp dt/2,
 // which is u + [(m - g)(u - u-) + Lk]/(m + g) without a division; A = 1 where no damping.
-#ifndef SWB_COMBINE
-#define SWB_COMBINE 0
-#endif
+// (measured alternatives: the increment formed first, or an E/D division instead of
+// the B field, gave the same accuracy once B's rounding is dithered, and the division costs 2-3 %)
 __device__ __forceinline__ float2 update2(float2 u, float2 um, float2 Lk, float2 a, float2 b) {
-#if SWB_COMBINE == 0
     return fma2(b, Lk, fma2(a, sub2(u, um), u));
-#elif SWB_COMBINE == 1
-    // increment first, one rounding at the scale of u
-    return add2(u, fma2(b, Lk, mul2(a, sub2(u, um))));
-#else
-    // fields D = m + g (slot b), E = m - g (slot a): u+ = u + (E (u - u-) + Lk) / D
-    return add2(u, div2(fma2(a, sub2(u, um), Lk), b));
-#endif
 }
 
 // Advance a ring position (stage, phase) by one.
@@ -176,9 +167,6 @@ __device__ __forceinline__ unsigned zmask_of(int zc, int z0, int z1) {
     return m;
 }
 
-#ifndef SWB_PRED_EVICT_LAST
-#define SWB_PRED_EVICT_LAST 0
-#endif
 // Store one output float4 row and fold it into the max|u| bits.  Full lanes take one
 // STG.128; boundary lanes predicated scalar stores; no per-element branches (the partial
 // case only exists on the first/last z tile).
@@ -213,13 +201,7 @@ __device__ __forceinline__ void store_row_pred(float* dst, const float4& o, unsi
         "setp.eq.u32 pf, %0, 15;\n\t"
         "setp.eq.u32 pl, %0, 3;\n\t"
         "setp.eq.u32 ph, %0, 12;\n\t"
-#if SWB_PRED_EVICT_LAST
-        ".reg .b64 pol;\n\t"
-        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-        "@pf st.global.L2::cache_hint.v4.f32 [%1], {%2, %3, %4, %5}, pol;\n\t"
-#else
         "@pf st.global.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
-#endif
         "@pl st.global.v2.f32 [%1], {%2, %3};\n\t"
         "@ph st.global.v2.f32 [%1+8], {%4, %5};\n\t"
         "}" ::"r"(zmask), "l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)
@@ -258,27 +240,6 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* flag, uns
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Intra-GPU progress wait (temporal blocking): gpu-scope acquire polls with a short backoff,
-// bounded at ~20 s (then records an error instead of hanging).  Returns the value seen.
-// No proxy fence here: the caller issues one fence.proxy.async after all its waits.
-__device__ __forceinline__ unsigned long long wait_gpu(const unsigned long long* flag, unsigned long long need,
-                                                       unsigned* err) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-    if (v < need) {
-        const unsigned long long t0 = gtimer();
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-            if (v >= need) break;
-            if (gtimer() - t0 > 20000000000ull) {
-                atomicExch(err, 1u);
-                break;
-            }
-        }
-    }
-    return v;
-}
-
 // End-of-CTA signal for the fused halo exchange (after the CTA barrier in block_max_commit).
 __device__ __forceinline__ void signal_neighbours(const Ctl& c) {
     if (threadIdx.x == 0 && (c.sig_lo || c.sig_hi)) {
@@ -304,21 +265,12 @@ inline cudaError_t launch_pdl_args(const void* fn, int grid, int threads, size_t
     cfg.numAttrs = 1;
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
-// k_sq kernels: (Maps, Geo, Coef, Ctl, Peer, Sched)
+// k_tma kernels: (Maps, Geo, Coef, Ctl, Peer, Sched)
 inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
                               const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
                               const Sched& sc) {
     void* args[] = {const_cast<Maps*>(&maps), const_cast<Geo*>(&g), const_cast<Coef*>(&K),
                     const_cast<Ctl*>(&c), const_cast<Peer*>(&p), const_cast<Sched*>(&sc)};
-    return launch_pdl_args(fn, grid, threads, smem, s, args);
-}
-// k_tma kernels: (Maps, Geo, Coef, Ctl, Peer, Sched, TbCtl)
-inline cudaError_t launch_pdl(const void* fn, int grid, int threads, size_t smem, cudaStream_t s,
-                              const Maps& maps, const Geo& g, const Coef& K, const Ctl& c, const Peer& p,
-                              const Sched& sc, const TbCtl& tb) {
-    void* args[] = {const_cast<Maps*>(&maps), const_cast<Geo*>(&g), const_cast<Coef*>(&K),
-                    const_cast<Ctl*>(&c), const_cast<Peer*>(&p), const_cast<Sched*>(&sc),
-                    const_cast<TbCtl*>(&tb)};
     return launch_pdl_args(fn, grid, threads, smem, s, args);
 }
 

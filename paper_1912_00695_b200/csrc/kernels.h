@@ -6,14 +6,6 @@
 
 namespace swb {
 
-// Temporal blocking (K3, two steps per launch): stage-1 progress counters, one per work item,
-// cumulative within a launch and tagged with the launch epoch in the high 32 bits.
-struct TbCtl {
-    unsigned long long* cnt;  // [items] device counters (null for single-step launches)
-    unsigned long long epoch; // launch sequence number (>= 1)
-    int ctas;                 // CTAs per stage; the grid is 2 * ctas
-};
-
 // SMs of the current device (cached per device; grid sizing of the element-wise kernels).
 int device_sm_count();
 
@@ -45,16 +37,8 @@ struct TmaPlan {
     int nchunk;           // dim-0 chunks per column
     const unsigned char* dflag;  // device [columns][planes] damp-tile-nonzero flags (or null)
     int variant;
-    int kind;             // 0: register-queue kernel (k_tma.cu), 1: smem-queue kernel (k_sq.cu)
-    // K3 schedule (two steps per launch): nchunk_tb dim-0 chunks so that 2 x items CTAs are
-    // co-resident (one per SM); tb_ok = 0 if the grid is too small for that.
-    int tb_ok;
-    int nchunk_tb;
-    int tb_items;
     int num_sms;
 };
-// CTAs per stage of a K3 launch (the grid is twice this).
-inline int tb_ctas(const TmaPlan& p) { return p.tb_items < p.num_sms / 2 ? p.tb_items : p.num_sms / 2; }
 // Host-side damp tile flags for a plan: flags[col * np + (x - x0)] = any damp != 0 in the tile.
 void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_local, int n1, int n2,
                     unsigned char* flags);
@@ -62,18 +46,16 @@ void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp_host_lo
 cudaError_t tma_damp_flags_device(const TmaPlan& plan, const Geo& g, unsigned char* flags, cudaStream_t s);
 TmaPlan tma_plan(int H, const Geo& g, int num_sms);
 // In place: m -> B = 1/(m + g), damp -> A = (m - g)/(m + g), g = fl(damp * half_dt), computed in
-// double and rounded once (cells with m == 0, row padding, get 0).  For K1 handles only.
-cudaError_t tma_update_coefs(float* m, float* damp, long long n, float half_dt, cudaStream_t s);
+// double and rounded once, to a neighbouring float chosen by a hash of the global cell index so
+// that the rounding is unbiased over a medium (cells with m == 0, row padding, get 0; A = 1 exactly
+// where g == 0).  For K1 handles only.  Buffer: [nl0][n1][P2], local plane 0 = global xg_off.
+cudaError_t tma_update_coefs(float* m, float* damp, long long n, float half_dt, int P2, int n1, int n2, int xg_off,
+                             cudaStream_t s);
 // Encodes the tensor maps for the three u levels (once per handle).
 constexpr int kTmaMapsBytes = 8 * 128;  // 8 CUtensorMaps
 cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* maps /*kTmaMapsBytes*/);
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s);
-// K3: steps c.step and c.step+1 in one launch (single domain, no linked neighbours); smax
-// slots c.slot and c.slot+1.
-cudaError_t launch_tma_tb(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
-                          const Ctl& c, const TbCtl& tb, cudaStream_t s);
-
 cudaError_t launch_ring_max(const float* u, long long plane, int P2, int nx0, int nx1, int n1,
                             int n2, int x_in0, int x_in1, int y_in0, int y_in1, int z_in0,
                             int z_in1, unsigned* out, cudaStream_t s);

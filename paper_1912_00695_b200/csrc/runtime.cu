@@ -131,7 +131,7 @@ struct swb_handle {
     int n0 = 0, n1 = 0, n2 = 0, so = 0, H = 0, HU = 0, P2 = 0;
     int lo = 0, hi = 0, gb = 0, ga = 0, nl0 = 0, xg_off = 0;
     long long plane = 0, level_floats = 0;
-    int form = 0, time_block = 1;
+    int form = 0;
     float* u = nullptr;
     float* m = nullptr;
     float* damp = nullptr;
@@ -170,8 +170,6 @@ struct swb_handle {
     alignas(128) unsigned char maps[kTmaMapsBytes];
     bool use_tma = false;
     unsigned char* d_dflag = nullptr;
-    unsigned long long* d_tbcnt = nullptr;  // K3 stage-1 progress counters [plan.tb_items]
-    unsigned long long tb_epoch = 0;         // K3 launches so far (counter tag)
     unsigned long long* d_trace = nullptr;  // SWB_TRACE: per-CTA timestamps of the last launch
     // halo links
     unsigned long long* d_flags = nullptr;   // [0]: written by lower neighbour, [1]: by upper
@@ -222,20 +220,6 @@ int setup_device(int device) {
         checked.fetch_or(bit);
     }
     SWB_CUDA(cudaSetDevice(device));
-    // L2 set-aside for persisting (evict_last) lines: the stencil stores u[t+1] with an evict_last
-    // policy so that the next step's u[t] reads hit L2.  SWB_L2_PERSIST=<MB> (0 = off) overrides
-    // (development).
-    static std::atomic<unsigned long long> l2set{0};
-    if (!(l2set.load() & bit)) {
-        int maxp = 0;
-        if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0) {
-            size_t want = static_cast<size_t>(maxp);
-            if (const char* e = std::getenv("SWB_L2_PERSIST")) want = std::min(want, static_cast<size_t>(std::atoll(e)) << 20);
-            else want = 0;
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) cudaGetLastError();
-        }
-        l2set.fetch_or(bit);
-    }
     return SWB_OK;
 }
 
@@ -332,37 +316,11 @@ int refresh_ring(swb_handle* h) {
 
 bool linked(const swb_handle* h) { return h->lo_remote || h->hi_remote || h->peer.lo_lev[0] || h->peer.hi_lev[0]; }
 
-// Temporal blocking applies to a single-domain TMA handle (slabs exchange halos every step).
-bool use_tb(const swb_handle* h) { return h->time_block >= 2 && h->use_tma && h->plan.tb_ok && h->d_tbcnt && !linked(h); }
 
 int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
     const int kmask = (h->lo_remote && !h->fused_lo ? 1 : 0) | (h->hi_remote && !h->fused_hi ? 2 : 0);
-    const bool tb = use_tb(h);
     for (int i = 0; i < nt;) {
         const int s = step0 + i;
-        if (tb && i + 1 < nt) {
-            // K3: steps s and s+1 in one launch, then both steps' receiver samples
-            Ctl c = h->ctl;
-            c.step = s;
-            c.slot = slot0 + i;
-            c.err = h->d_err;
-            c.ghost_lo_end = 0;
-            c.ghost_hi_begin = INT_MAX;
-            TbCtl t{};
-            t.cnt = h->d_tbcnt;
-            t.epoch = ++h->tb_epoch;
-            SWB_CUDA(launch_tma_tb(h->plan, h->maps, h->geo, h->K, c, t, h->stream));
-            ++h->launches;
-            for (int k = 0; k < 2 && !h->rec_owned.empty(); ++k) {
-                const int owned = static_cast<int>(h->rec_owned.size());
-                SWB_CUDA(launch_samplers(h->u + ((s + k + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w,
-                                         owned, h->d_traces + static_cast<long long>(slot0 + i + k) * owned,
-                                         h->stream));
-                ++h->launches;
-            }
-            i += 2;
-            continue;
-        }
         if (kmask) {  // kernel-based ordering for sides without fused support
             SWB_CUDA(launch_wait_flags(h->d_flags, kmask, h->steps_done + i, h->d_err, h->stream));
             ++h->launches;
@@ -413,7 +371,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
     return SWB_OK;
 }
 
-bool fused_capable(const swb_handle* h) { return h->use_tma && h->plan.kind == 0; }
+bool fused_capable(const swb_handle* h) { return h->use_tma; }
 
 void compute_peer_ranges(swb_handle* h) {
     // planes mirrored to the lower neighbour: global [lo, lo+HU) ∩ updated; upper: [hi-HU, hi) ∩ updated
@@ -460,8 +418,9 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     if (!(p->dt > 0.0f)) return fail(SWB_EINVAL, "dt must be positive");
     if (!p->m && !p->velocity) return fail(SWB_EINVAL, "m (squared slowness) or the velocity is required");
     if (p->form < 0 || p->form > 4) return fail(SWB_EINVAL, "unknown stencil form");
-    if (p->time_block < 0 || p->time_block > 2)
-        return fail(SWB_EINVAL, "time_block must be 1 (one step per launch) or 2 (temporal blocking)");
+    if (p->time_block < 0 || p->time_block > 1)
+        return fail(SWB_EINVAL, "time_block must be 1: the temporal-blocking kernel (two steps per launch) was "
+                                "measured 0.53-0.74x of the single-step kernel on B200 and is retired (DESIGN.md)");
     const int HU = p->space_order / 2;
     const int H = std::max(HU, 1);  // widest halo among u (SO/2), m and damp (1): src/pipeline.cpp:79-88
     const char* dn[3] = {"x", "y", "z"};
@@ -532,7 +491,6 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     h->plane = static_cast<long long>(h->n1) * h->P2;
     h->level_floats = h->plane * h->nl0;
     h->form = p->form;
-    h->time_block = std::max(1, p->time_block);
 
     auto cleanup = [&](int code) {
         swb_destroy(h);
@@ -766,12 +724,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
             h->use_tma = true;
             // K1 reads m and damp only as the update coefficients B = 1/(m+g), A = (m-g)/(m+g):
             // transform them in place (after the damp flags above, same stream)
-            if (h->plan.kind == 0)
-                SWB_CUDA_C(tma_update_coefs(h->m, h->damp, h->level_floats, h->K.half_dt, h->stream));
-            if (h->time_block >= 2 && h->plan.tb_ok) {
-                SWB_CUDA_C(hbuf_alloc(h, &h->d_tbcnt, sizeof(unsigned long long) * h->plan.tb_items));
-                SWB_CUDA_C(cudaMemsetAsync(h->d_tbcnt, 0, sizeof(unsigned long long) * h->plan.tb_items, h->stream));
-            }
+            SWB_CUDA_C(tma_update_coefs(h->m, h->damp, h->level_floats, h->K.half_dt, h->P2, h->n1, h->n2,
+                                            h->xg_off, h->stream));
         }
     }
     h->stats.kernel_variant = h->use_tma ? h->plan.variant : 100 + h->form;
@@ -779,8 +733,7 @@ int swb_create(const swb_problem* p, swb_handle** out) {
         SWB_CUDA_C(cudaMalloc(&h->d_trace, sizeof(unsigned long long) * 4 * 1024));
         h->ctl.trace = h->d_trace;
     }
-    h->stats.launch_steps = (h->time_block >= 2 && h->use_tma && h->plan.tb_ok) ? 2 : 1;
-    if (h->stats.launch_steps == 2) h->stats.kernel_variant += 10000;  // K3 (two-step) variant ids
+    h->stats.launch_steps = 1;
     compute_peer_ranges(h);
     mark("plan+maps+dflags");
     SWB_CUDA_C(cudaStreamSynchronize(h->stream));
@@ -851,30 +804,10 @@ int swb_apply_async(swb_handle* h, int step0, int nt) {
     if (nt > 0) SWB_CUDA(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned) * nt, h->stream));
     h->launches = 0;
     h->ctl.smax = h->d_smax;
-    // SWB_GRAPH=1: capture the step loop into a CUDA graph (programmatic edges kept) and launch
-    // it as one unit; the capture/instantiation is host work outside the timed events.
-    // Single-domain, single-step launches only (K3 epochs and slab counters are host state).
-    static const bool use_graph = std::getenv("SWB_GRAPH") != nullptr;
-    if (use_graph && !linked(h) && !use_tb(h) && nt > 0) {
-        cudaGraph_t graph = nullptr;
-        cudaGraphExec_t exec = nullptr;
-        SWB_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        rc = enqueue_steps(h, step0, nt);
-        cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
-        if (rc) return rc;
-        SWB_CUDA(e);
-        SWB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
-        SWB_CUDA(cudaGraphLaunch(exec, h->stream));
-        SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
-        cudaGraphExecDestroy(exec);  // released once the launch completes
-        cudaGraphDestroy(graph);
-    } else {
-        SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
-        rc = enqueue_steps(h, step0, nt);
-        if (rc) return rc;
-        SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
-    }
+    SWB_CUDA(cudaEventRecord(h->ev0, h->stream));
+    rc = enqueue_steps(h, step0, nt);
+    if (rc) return rc;
+    SWB_CUDA(cudaEventRecord(h->ev1, h->stream));
     h->pend_step0 = step0;
     h->pend_nt = nt;
     h->pending = true;
@@ -1213,7 +1146,6 @@ int swb_link_local(swb_handle* lower, swb_handle* upper) {
     upper->peer_dev_lo = lower->device;
     lower->nb_grid_hi = upper->plan.grid;
     upper->nb_grid_lo = lower->plan.grid;
-    lower->stats.launch_steps = upper->stats.launch_steps = 1;  // linked slabs step one at a time
     compute_peer_ranges(lower);
     compute_peer_ranges(upper);
     return SWB_OK;
@@ -1289,7 +1221,6 @@ int swb_link_neighbours(swb_handle* h, const void* lower_blob, size_t lower_len,
         h->nb_grid_hi = b.grid;
         h->peer_dev_hi = device_of_uuid(b.uuid);
     }
-    h->stats.launch_steps = 1;  // linked slabs step one at a time
     compute_peer_ranges(h);
     return SWB_OK;
 }

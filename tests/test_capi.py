@@ -138,7 +138,7 @@ def _raw_problem(shape=(16, 16, 16), so=4, **kw):
     p.form = 0
     p.time_block = 1
     for k, v in kw.items():
-        setattr(p, k, v)
+        setattr(p, k, N.fptr(None) if v is None else v)
     return p, m
 
 
@@ -147,6 +147,8 @@ def _raw_problem(shape=(16, 16, 16), so=4, **kw):
     (dict(so=26), "space_order above 24"),
     (dict(shape=(8, 16, 16), so=8), "too small for halo"),
     (dict(time_block=3), "time_block must be 1"),
+    (dict(time_block=2), "is retired"),
+    (dict(m=None), "or the velocity is required"),
     (dict(form=9), "unknown stencil form"),
     (dict(dt=0.0), "dt must be positive"),
     (dict(slab_lo=0, slab_hi=3, so=8), "slab thinner than SO/2 planes"),

@@ -65,37 +65,23 @@ def test_smallest_grids(so):
     assert rel_l2(fast.u.data[fl], ref["levels"][fl]) <= 1e-5
 
 
-@pytest.mark.parametrize("so", [4, 8, 16])
-def test_smem_queue_kernel_variant(so, monkeypatch):
-    """The shared-memory-queue TMA kernel (k_sq.cu, SWB_KERNEL=sq; slower than the register
-    queue, kept for comparison) is a valid factorised kernel: <= 1e-5 against the oracle."""
-    monkeypatch.setenv("SWB_KERNEL", "sq")
-    shape, nt = (44, 46, 70), 30
-    prob, ocfg = _pair(shape, so, nt, seed=so)
-    ref = O.port_run(ocfg)
-    op = P.Operator(prob)
-    assert op.stats().kernel_variant == 2000 + so // 2
-    op.apply(nt, 0)
-    fl = nt % 3
-    assert rel_l2(op.get_level(fl), ref["levels"][fl]) <= 1e-5
-
-
 def test_handles_recycled_through_the_buffer_pool():
     """Every device buffer of a handle (fields, counters, flags, traces) is recycled through the
-    process-wide pool on destroy.  Interleaved handles of two problems, with receivers, damping
-    and temporal blocking, must reproduce their first results bit for bit on every reuse."""
+    process-wide pool on destroy.  Interleaved handles of two problems and two forms, with
+    receivers and damping, must reproduce their first results bit for bit on every reuse."""
     def make(shape, so, seed):
         rng = np.random.default_rng(seed)
         vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
         return P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
                                                        steps=9, velocity_field=vel, damp_max=0.05,
                                                        damp_width=4))
-    cases = [(make((36, 40, 70), 8, 1), 1), (make((30, 34, 44), 4, 2), 2), (make((36, 40, 70), 8, 1), 2)]
+    cases = [(make((36, 40, 70), 8, 1), "factorised"), (make((30, 34, 44), 4, 2), "factorised"),
+             (make((36, 40, 70), 8, 1), "plain_f64")]
     first = {}
     for rnd in range(4):
-        for ci, (prob, tb) in enumerate(cases):
+        for ci, (prob, form) in enumerate(cases):
             rec = np.array([[x, 12, 20] for x in range(4, prob.shape[0] - 4, 5)], np.int32)
-            op = P.Operator(prob, time_block=tb, receivers=rec)
+            op = P.Operator(prob, form=form, receivers=rec)
             r = op.apply(9, 0)
             got = (op.levels().copy(), np.asarray(r.step_max_abs).copy(), np.asarray(r.rec_traces).copy())
             op.close()
@@ -104,6 +90,6 @@ def test_handles_recycled_through_the_buffer_pool():
             else:
                 for a, b in zip(first[ci], got):
                     assert np.array_equal(a, b), (rnd, ci)
-    # K1 and K3 on the same problem agree as well
-    for a, b in zip(first[0], first[2]):
-        assert np.array_equal(a, b)
+    # the two forms on the same problem agree to the north-star tolerance
+    fl = 9 % 3
+    assert rel_l2(first[0][0][fl], first[2][0][fl]) <= 1e-5

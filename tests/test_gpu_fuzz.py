@@ -51,13 +51,6 @@ def test_random_configuration(seed):
     fl = fast.final_level
     assert rel_l2(fast.u.data[fl], ref["levels"][fl]) <= 1e-5
     assert rel_l2(fast.rec_traces, ref["rec_traces"]) <= 1e-5
-    # temporal blocking runs the same per-point arithmetic
-    op = P.Operator(prob, time_block=2, receivers=rec)
-    for l in range(3):
-        op.set_level(l, init[l])
-    r3 = op.apply(nt, 0)
-    assert np.array_equal(op.levels(), fast.u.data)
-    assert np.array_equal(r3.rec_traces, fast.rec_traces)
 
 
 @pytest.mark.parametrize("seed", range(16))

@@ -229,10 +229,9 @@ def test_offgrid_receivers_trilinear(form):
         P.Operator(P.make_wave_problem(cfg), receiver_coords=[[-1.0, 5.0, 5.0]])
 
 
-@pytest.mark.parametrize("time_block", [1, 2])
 @pytest.mark.parametrize("so", [4, 8, 12, 16])
 @pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
-def test_nonfinite_detected_by_fused_max(so, bad, time_block):
+def test_nonfinite_detected_by_fused_max(so, bad):
     """The factorised kernels fold max|u| in their epilogue (FMNMX3.NAN on |u|); a non-finite
     value must surface as InstabilityError at the first step whose newest level holds it, as
     max_abs_interior does (src/executor.cpp:526-544, 588-593).  A NaN/inf placed in the
@@ -240,7 +239,7 @@ def test_nonfinite_detected_by_fused_max(so, bad, time_block):
     shape = (40, 42, 70)
     prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0),
                                                    space_order=so, steps=6))
-    op = P.Operator(prob, form="factorised", time_block=time_block)
+    op = P.Operator(prob, form="factorised")
     u0 = np.zeros(shape, np.float32)
     u0[20, 21, 33] = bad
     op.set_level(0, u0)
