@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer over every kernel family (scripts/sanitize_cases.py); logs in gpurun_out/sanitize_*.log
+# (summaries copied to profiles/sanitize_r02.txt).  Each tool reports "ERROR SUMMARY: 0 errors" when clean.
+mkdir -p gpurun_out
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck synccheck racecheck initcheck; do
+  for case in k1 simple slabs extras; do
+    timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 python scripts/sanitize_cases.py $case \
+        > gpurun_out/sanitize_${tool}_${case}.log 2>&1
+    echo "$tool $case rc=$? $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY' gpurun_out/sanitize_${tool}_${case}.log | tail -1)"
+  done
+done
