@@ -4,7 +4,10 @@
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck synccheck racecheck initcheck; do
-  for case in k1 simple slabs extras; do
+  cases="k1 simple slabs extras"
+  # initcheck serialises co-resident grids: the fused-ordering slabs would hit their 20 s bounded wait
+  [ $tool = initcheck ] && cases="k1 simple slabs_ordered extras"
+  for case in $cases; do
     timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 python scripts/sanitize_cases.py $case \
         > gpurun_out/sanitize_${tool}_${case}.log 2>&1
     echo "$tool $case rc=$? $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY' gpurun_out/sanitize_${tool}_${case}.log | tail -1)"
