@@ -62,10 +62,19 @@ def extras():
 
 
 def slabs_ordered():
-    """Kernel-ordered exchange only: initcheck serialises the two co-resident persistent grids that
-    the fused in-kernel ordering needs, so under initcheck their bounded waits time out (by design,
-    an error instead of a hang) and the fused mode is covered by memcheck/synccheck/racecheck."""
-    slabs((False,))
+    """Kernel-ordered exchange under initcheck.  initcheck serialises the slabs' streams, so a slab
+    whose wait kernel spins for a neighbour would block that neighbour (and time out by design); the
+    slabs are therefore stepped round-robin, one synchronous step each, which satisfies every wait
+    before it is issued.  The fused in-kernel ordering is covered by memcheck/synccheck/racecheck."""
+    pr = prob((40, 30, 70), 8, 6)
+    ops = [P.Operator(pr, slab=s) for s in ((0, 14), (14, 27), (27, 40))]
+    P.Operator.link_local(ops[0], ops[1])
+    P.Operator.link_local(ops[1], ops[2])
+    for step in range(6):
+        for o in ops:
+            o.apply(1, step)
+    for o in ops:
+        o.close()
 
 
 CASES = {"k1": k1, "simple": simple, "slabs": slabs, "slabs_ordered": slabs_ordered, "extras": extras}
