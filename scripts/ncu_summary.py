@@ -67,6 +67,11 @@ if __name__ == "__main__":
     if tb:
         summ, lines = main(tag, tb, pts, key="k_tma_tb", steps=2, summ=summ, lines=lines)
     text = "\n".join(lines) + "\n"
-    json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
+    # merge: keep the other captures' keys (steady-state ranges, retired-kernel history)
+    old = json.load(open("profiles/ncu_summary.json")) if os.path.exists("profiles/ncu_summary.json") else {}
+    if "k_tma" in old and old.get("tag") != tag:
+        old[f"k_tma_{old.get('tag', 'prev')}"] = old["k_tma"]
+    old.update(summ)
+    json.dump(old, open("profiles/ncu_summary.json", "w"), indent=1)
     open(f"profiles/ncu_k_tma_{tag}.txt", "w").write(text)
     print(text)

@@ -2,7 +2,6 @@
 # ncu evidence for the stencil kernels (run under gpurun; one GPU).
 #  1. launch list of the bench command (per-kernel share of the step)
 #  2. one --set full capture of K1 (k_tma, one step per launch) per space order
-#  3. one --set full capture of K3 (k_tma<...,1>, two steps per launch) at SO 4 / 8 / 16
 set -x
 mkdir -p gpurun_out
 # the driver's default bench command; ncu records the first 400 kernel launches (setup, the
@@ -12,8 +11,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 for so in ${SOS:-4 8 12 16}; do
   ncu --set full --clock-control none --import-source on -k regex:k_tma -s 6 -c 1 \
       -o gpurun_out/tma_so$so python scripts/probe_perf.py factorised $so 256 8 > gpurun_out/ncu_so$so.log 2>&1
-done
-for so in ${TBSOS:-4 8 16}; do
-  TB=2 ncu --set full --clock-control none --import-source on -k regex:k_tma -s 4 -c 1 \
-      -o gpurun_out/tb_so$so python scripts/probe_perf.py factorised $so 256 8 > gpurun_out/ncu_tb_so$so.log 2>&1
 done
