@@ -7,7 +7,8 @@ driver's headline is bench.py).  Writes gpurun_out/configs.json.
   3  256^3 SO 8/16: plain (basic DSE) FP32 and FP64 vs factorised -- GPts/s, reference flop
      counts, GFLOP/s (DRAM bytes per point come from ncu, profiles/)
   4  512^3 SO 8 with a damping layer (damp_width 10, damp_max 2e-5... as chosen below), 1 GPU
-  5  512^3 SO 16 per GPU: K3 (time_block=2) vs K1, 1 GPU
+  5  512^3 SO 16 per GPU (K1; the temporal-blocking K3 was retired), 1 GPU, and
+     512^3 at the other space orders
 """
 import json, sys, time
 import numpy as np
@@ -70,7 +71,8 @@ out["config4_512cube_so8_damped_1gpu_gpts"] = {"damp_width": 10, "damp_max": dm,
                                                "gpts": gpts((512,) * 3, 8, 200, damp_max=dm, damp_width=10),
                                                "undamped_gpts": gpts((512,) * 3, 8, 200)}
 # ---- config 5 ----
-out["config5_512cube_so16_1gpu_gpts"] = {"k1": gpts((512,) * 3, 16, 100), "k3_time_block2": gpts((512,) * 3, 16, 100, tb=2)}
+out["config5_512cube_so16_1gpu_gpts"] = {"k1": gpts((512,) * 3, 16, 100)}
+out["k1_512cube_gpts"] = {f"so{s}": gpts((512,) * 3, s, 100) for s in (4, 8, 12, 16)}
 print(json.dumps(out, indent=1))
 import os
 os.makedirs("gpurun_out", exist_ok=True)
