@@ -619,6 +619,12 @@ const Variant* find_variant(int H, int t1_want = 0) {
     return nullptr;
 }
 
+// A variant with exactly this tile height exists for the halo (rows-per-thread preference applied).
+bool find_variant_exact_t1(int H, int t1) {
+    const Variant* v = find_variant(H, t1);
+    return v && v->T1 == t1;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -657,16 +663,44 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     p.ok = 0;
     p.H = H;
     p.num_sms = num_sms;
-    // Tile height: among the K1 heights for this halo, the one whose row tiles waste the fewest
-    // rows of the interior (measured +1-2 % at 256^3 SO 4/8/12 and 512^3 SO 8 over a fixed
-    // height; heights below 28 lose warps and are not auto-selected).
-    int t1_best = 0;
-    double eff_best = -1.0;
+    // Tile height and dim-0 chunk count together: among the K1 heights for this halo (28/30 rows at
+    // SO <= 12, 20/22 at SO 14-16), the pair with the smallest estimated makespan
+    //     rounds(columns x chunks over the persistent CTAs) x (chunk length + warm-up) x t(T1),
+    // where t(T1) ~ T1^0.25 is the time a CTA takes per plane of a T1-row tile (measured: a 20-row
+    // SO 16 tile streams a plane 2.3 % faster than a 22-row one; the kernel is shared-memory and
+    // latency bound, not proportional to rows).  At 256^3 SO 16 this picks 20 rows: 48 columns x 3
+    // chunks fill 144 of 148 SMs instead of 132 (+2.4 %); at 512^3 it keeps 22 (20 rows: -8 %).
+    // Ties go to the height that wastes fewer interior rows.  SWB_TPLAN=rows: row efficiency only
+    // (the previous rule, development A/B).
     const int rows = g.y1 - g.y0;
-    for (int cand : {30, 28, 22}) {
+    const int np_all = g.x1 - g.x0;
+    const int zs_all = g.z0 & ~3;
+    const int tz_all = ceil_div(g.z1 - zs_all, kT2);
+    const bool rows_only = std::getenv("SWB_TPLAN") && std::strcmp(std::getenv("SWB_TPLAN"), "rows") == 0;
+    auto makespan = [&](int t1, int* nchunk_out) {
+        const long long cols = static_cast<long long>(ceil_div(rows, t1)) * tz_all;
+        double best_cost = 1e300;
+        int best_nc = 1;
+        for (int nc = 1; nc <= 32 && nc <= std::max(np_all, 1); ++nc) {
+            const long long rounds = (cols * nc + num_sms - 1) / num_sms;
+            const double cost = static_cast<double>(rounds) * (std::ceil(static_cast<double>(np_all) / nc) + H);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best_nc = nc;
+            }
+        }
+        if (nchunk_out) *nchunk_out = best_nc;
+        return best_cost * std::pow(static_cast<double>(t1), 0.25);
+    };
+    int t1_best = 0;
+    double eff_best = -1.0, cost_best = 1e300;
+    for (int cand : {30, 28, 22, 20}) {
         if ((H <= 6) != (cand >= 28)) continue;
+        if (!find_variant_exact_t1(H, cand)) continue;
         const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
-        if (eff > eff_best + 1e-9) {
+        const double cost = rows_only || np_all <= 0 || rows <= 0 ? 0.0 : makespan(cand, nullptr);
+        if (cost < cost_best * (1 - 1e-9) || (cost <= cost_best * (1 + 1e-9) && eff > eff_best + 1e-9)) {
+            cost_best = cost;
             eff_best = eff;
             t1_best = cand;
         }
