@@ -99,7 +99,7 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
                 if constexpr (H % 4 != 0)
                     store_row_pred(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
                 else
-                    store_row(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
+                    store_row<true>(un + xoff + static_cast<long long>(i) * g.P2, out[i], it.zmask, mine);
             }
     } else {
         // slab-boundary planes (also stored into the neighbour's ghost plane, 128-bit, same

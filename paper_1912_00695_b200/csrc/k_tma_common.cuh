@@ -170,15 +170,26 @@ __device__ __forceinline__ unsigned zmask_of(int zc, int z0, int z1) {
 // Store one output float4 row and fold it into the max|u| bits.  Full lanes take one
 // STG.128; boundary lanes predicated scalar stores; no per-element branches (the partial
 // case only exists on the first/last z tile).
+// kHoist: the L2 policy comes from a non-volatile asm with no inputs, so it is computed once and
+// hoisted out of the plane loop (2 registers) instead of rebuilt by ~6 uniform ops at every
+// store; the plain-store plane path of the variants with H % 4 == 0 takes it.
+template <bool kHoist = false>
 __device__ __forceinline__ void store_row(float* dst, const float4& o, unsigned zmask, unsigned& mine) {
     if (zmask == 0xFu) {
         // u[t+1] is next step's u[t] (halo re-reads by the neighbouring tiles): keep it in L2
         // (evict_last; measured +1.1 % at SO 8, neutral on the predicated-store variants)
-        asm volatile(
-            "{\n\t.reg .b64 pol;\n\t"
-            "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-            "st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, pol;\n\t}"
-            ::"l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w) : "memory");
+        if constexpr (kHoist) {
+            uint64_t pol;
+            asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                         ::"l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w), "l"(pol) : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .b64 pol;\n\t"
+                "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                "st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, pol;\n\t}"
+                ::"l"(dst), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w) : "memory");
+        }
         mine = fold_abs4(mine, o.x, o.y, o.z, o.w);
     } else if (zmask) {
         if (zmask & 1u) dst[0] = o.x;
