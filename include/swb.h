@@ -229,8 +229,9 @@ int swb_damp_data(const int32_t* shape, float damp_max, int damp_width, float* o
 const char* swb_version(void);
 
 /* Debug: with SWB_TRACE=1 in the environment at swb_create, copy the per-CTA globaltimer
- * stamps [cta][start, warm-up done, compute done, exit] of the last stencil launch.
- * Returns the number of CTAs of that launch (or a negative error). */
+ * stamps of the last K1 launch of an even and of an odd step: out[parity][cta][8] =
+ * {entry, after griddepcontrol.wait, warm-up done, compute done, exit, 0, 0, 0}
+ * (out holds 2 * 8 * max_ctas values).  Returns the number of CTAs (or a negative error). */
 int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas);
 
 #ifdef __cplusplus

@@ -358,6 +358,10 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    // per-CTA stamps (SWB_TRACE): [entry, after griddepcontrol.wait, warm-up done, consumers done,
+    // exit] of the last two launches (even / odd step)
+    unsigned long long* tr = c.trace ? c.trace + 8 * (blockIdx.x + 1024 * (c.step & 1)) : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
     // Programmatic dependent launch: everything above overlapped the previous step's tail;
     // u[t], u[t-1] written by that step are only touched after this point.
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -366,7 +370,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     const int nitems = sc.ncol * sc.nchunk;
     const int first = static_cast<int>(blockIdx.x), G = static_cast<int>(gridDim.x);  // persistent CTAs
     unsigned mine = 0u;
-    if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x] = gtimer();
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
     if (warp == 0) {
         // ===== TMA producers: lane 0 feeds the u ring, lane 1 the aux ring, each limited
@@ -485,11 +489,11 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
             it.xrun = static_cast<long long>(it.q0 + it.dir * H) * g.plane + it.gcol;  // first output plane
             sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
-            if (c.trace && ct == 0 && item == first) {
+            if (tr && ct == 0 && item == first) {
                 // time when the first output plane's data is complete (end of warm-up)
                 unsigned s2 = (su + 2 * H) % SU, p2 = pu ^ (((su + 2 * H) / SU) & 1u);
                 mbar_wait(full_u + 8 * s2, p2);
-                c.trace[4 * blockIdx.x + 1] = gtimer();
+                tr[2] = gtimer();
             }
             if constexpr (kUnroll) {
 #pragma unroll 1
@@ -518,10 +522,10 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     // (peer stores reach system scope through thread 0's __threadfence_system in
     // signal_neighbours, after the CTA barrier in block_max_commit: fence cumulativity)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (c.trace && threadIdx.x == 32) c.trace[4 * blockIdx.x + 2] = gtimer();
+    if (tr && threadIdx.x == 32) tr[3] = gtimer();
     block_max_commit(mine, c.smax + c.slot);  // (contains the CTA barrier)
     signal_neighbours(c);
-    if (c.trace && threadIdx.x == 0) c.trace[4 * blockIdx.x + 3] = gtimer();
+    if (tr && threadIdx.x == 0) tr[4] = gtimer();
 }
 
 template <int H, int R1, int T1, int SU, int SA, int UNR>

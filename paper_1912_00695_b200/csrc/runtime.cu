@@ -730,7 +730,8 @@ int swb_create(const swb_problem* p, swb_handle** out) {
     }
     h->stats.kernel_variant = h->use_tma ? h->plan.variant : 100 + h->form;
     if (std::getenv("SWB_TRACE") && h->use_tma) {
-        SWB_CUDA_C(cudaMalloc(&h->d_trace, sizeof(unsigned long long) * 4 * 1024));
+        SWB_CUDA_C(cudaMalloc(&h->d_trace, sizeof(unsigned long long) * 2 * 8 * 1024));
+        SWB_CUDA_C(cudaMemset(h->d_trace, 0, sizeof(unsigned long long) * 2 * 8 * 1024));
         h->ctl.trace = h->d_trace;
     }
     h->stats.launch_steps = 1;
@@ -1053,7 +1054,9 @@ int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas) {
     if (!h || !h->d_trace) return fail(SWB_EINVAL, "tracing not enabled (set SWB_TRACE=1)");
     SWB_CUDA(cudaStreamSynchronize(h->stream));
     const int n = std::min(max_ctas, 1024);
-    SWB_CUDA(cudaMemcpy(out, h->d_trace, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
+    for (int par = 0; par < 2; ++par)
+        SWB_CUDA(cudaMemcpy(out + static_cast<size_t>(par) * 8 * n, h->d_trace + static_cast<size_t>(par) * 8 * 1024,
+                            sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost));
     return h->plan.grid;
 }
 
