@@ -3,7 +3,8 @@
 // One persistent CTA per SM strides over work items (column tile x dim-0 chunk): a column
 // tile is T1 rows (dim 1) x 64 cols (dim 2) of output points; the CTA streams it along dim 0
 // (the reference's slowest axis "x"; the north star's "z-slab" axis) over the chunk's planes.
-// Warp 0 is the TMA producer (lane 0: u ring, lane 1: aux ring); warps 1..NCW are consumers.
+// Warp 0 is the TMA producer (lane 0: u ring, lane 1: aux ring); warps 1..NCW are consumers;
+// the SO 16 20-row variant adds one y-pencil warp (far y terms, see ypencil_loop).
 //
 //   u ring  : halo-padded planes of u[t] ((T1+2H) x (64+2A) floats) loaded by
 //             cp.async.bulk.tensor.3d; a plane stays resident from its arrival (when the
@@ -125,7 +126,85 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
     }
 }
 
-template <int H, int R1, int T1, int SU, int SA, int QN, int U>
+// ---- y-pencil warp (variants with YW = 1; SO 16 on grids where the 20-row tile is chosen) ----
+// The consumers are bound by shared-memory traffic and latency at SO 16: per output float4 they
+// issue 2H LDS.128 for the y neighbours alone.  A pencil warp takes the far y terms k >= kP of
+// every output plane:
+//   P_y = sum_{k=H..kP} c_k (u_{y-k} + u_{y+k})                                       FP32
+// Each lane owns one float4 column and half of the tile rows and holds its whole pencil (T1/2 + 2H
+// rows) in registers, so every u value is read from shared memory once per pencil instead of once
+// per output that needs it; P_y goes to a two-stage ring and the consumers read it with one
+// LDS.128 in place of 2 (H - kP + 1) loads.  kP balances the pencil warp (one warp per CTA, its
+// FFMA2 chains are the bound) against the consumers; measured at SO 16 on B200 (256^3, 20-row tile,
+// GPts/s): kP = 3: 202, 4: 209, 5: 219, 6: 214, 7: 209, 8: 201, no pencil 208.5
+// (profiles/pencil_r02.txt).
+template <int H>
+constexpr int pencil_k() { return H - 3; }
+
+struct YRing {
+    unsigned full, empty;  // mbarriers of stage 0 (8 bytes apart)
+    const float* col;      // this consumer's float4 in stage 0
+    unsigned st, ph;       // consumer's stage / phase
+};
+
+// Pencil warp yw (of YW) takes output planes g = yw, yw + YW, ... of this CTA in the consumers'
+// order.  The consumers wait for P_y of output plane p before they release p's u-ring stage, so
+// the pencil's reads of that stage are ordered before the TMA overwrite (mbarrier release/acquire).
+template <int H, int T1, int SU, int SS, int YW>
+__device__ __forceinline__ void ypencil_loop(int yw, int lane, const unsigned char* uring, float* sring,
+                                             unsigned full_u, unsigned full_s, unsigned empty_s,
+                                             const Coef& K, const Sched& sc, int first, int G, int nitems) {
+    using C = Cfg<H, 1, T1, YW>;
+    constexpr int SEG = T1 / 2;
+    constexpr int NL = SEG + 2 * H;
+    constexpr int KP = pencil_k<H>();
+    static_assert(T1 % 2 == 0 && KP >= 2, "two pencils per column; k = 1 stays with the consumers");
+    const int tz = lane & 15, seg = lane >> 4;
+    const float* ub = reinterpret_cast<const float*>(uring) + seg * SEG * C::W2 + C::A + 4 * tz;
+    float* sb = sring + seg * SEG * kT2 + 4 * tz;
+    unsigned gseq = 0, useq = 0;  // output planes / u-ring planes of the items before this one
+    for (int item = first; item < nitems; item += G) {
+        const int chunk = item / sc.ncol;
+        const int xa = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * chunk / sc.nchunk);
+        const int xb = sc.x0 + static_cast<int>(static_cast<long long>(sc.np) * (chunk + 1) / sc.nchunk);
+        const int np = xb - xa;
+#pragma unroll 1
+        for (int j = static_cast<int>((yw + YW - gseq % YW) % YW); j < np; j += YW) {
+            const unsigned gs = gseq + j, us = useq + j + H;  // output plane j is u-ring plane j + H
+            const unsigned sst = gs % SS, sph = (gs / SS) & 1u;
+            const unsigned ust = us % SU, uph = (us / SU) & 1u;
+            mbar_wait(empty_s + 8 * sst, sph ^ 1u);
+            mbar_wait(full_u + 8 * ust, uph);
+            const float* pl = ub + ust * (C::UPLANE / 4);
+            float* so = sb + sst * (T1 * kT2);
+            // all NL rows first (no queue here: registers to spare), then k outer / outputs inner,
+            // so SEG independent FFMA2 chains advance together
+            float4 v[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) v[i] = *reinterpret_cast<const float4*>(pl + i * C::W2);
+            float2 al[SEG], ah[SEG];
+#pragma unroll
+            for (int o = 0; o < SEG; ++o) al[o] = ah[o] = splat(0.f);
+#pragma unroll
+            for (int k = H; k >= KP; --k) {
+                const float2 ck = splat(K.c[k]);
+#pragma unroll
+                for (int o = 0; o < SEG; ++o) {  // output row o of the pencil: centre v[o + H]
+                    al[o] = fma2(ck, add2(lo2(v[o + H - k]), lo2(v[o + H + k])), al[o]);
+                    ah[o] = fma2(ck, add2(hi2(v[o + H - k]), hi2(v[o + H + k])), ah[o]);
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < SEG; ++o)
+                *reinterpret_cast<float4*>(so + o * kT2) = make_float4(al[o].x, al[o].y, ah[o].x, ah[o].y);
+            mbar_arrive(full_s + 8 * sst);  // release: this lane's P_y stores
+        }
+        gseq += np;
+        useq += np + 2 * H;
+    }
+}
+
+template <int H, int R1, int T1, int SU, int SA, int QN, int U, int YW, int SS>
 __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& it,
                                               const float* ucol, const float* acol,
                                               const unsigned* aflag, unsigned full_u,
@@ -134,8 +213,8 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
                                               unsigned& sa, unsigned& pa_, unsigned& mine,
                                               float* un, float* lo_peer, float* hi_peer,
                                               const Geo& g, const Coef& K, const Ctl& c,
-                                              const Peer& pr) {
-    using C = Cfg<H, R1, T1>;
+                                              const Peer& pr, YRing& yr) {
+    using C = Cfg<H, R1, T1, YW>;
     constexpr int NQ = QN;  // queue slots; plane j-m sits in slot (U - m) mod QN
     const int q = it.q0 + it.dir * j;
     mbar_wait(full_u + 8 * su, pu);
@@ -162,12 +241,29 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
 #pragma unroll
         for (int k = H; k >= 2; --k) {
             const float2 ck = splat(K.c[k]);
-            const float4 ym = *reinterpret_cast<const float4*>(rowc - k * C::W2);
-            const float4 yp = *reinterpret_cast<const float4*>(rowc + k * C::W2);
+            // far y pairs k >= pencil_k come from the pencil warp (P_y); the loads are issued first,
+            // as in the variants without it (the register-capped SO 12 variant is sensitive to it)
+            const bool from_pencil = YW > 0 && k >= pencil_k<H>();
+            const float4 ym = from_pencil ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                          : *reinterpret_cast<const float4*>(rowc - k * C::W2);
+            const float4 yp = from_pencil ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                          : *reinterpret_cast<const float4*>(rowc + k * C::W2);
             const float4& xm = Q[i][(UC + NQ - k) % NQ];
             const float4& xp = Q[i][(UC + k) % NQ];
             float2 sl, sh;
-            if constexpr (kLap == 2) {
+            if (from_pencil) {
+                float2 zl, zh;
+                if ((k & 1) == 0) {
+                    zl = add2(make_float2(w[C::A - k], w[C::A + 1 - k]), make_float2(w[C::A + k], w[C::A + 1 + k]));
+                    zh = add2(make_float2(w[C::A + 2 - k], w[C::A + 3 - k]),
+                              make_float2(w[C::A + 2 + k], w[C::A + 3 + k]));
+                } else {
+                    zl = make_float2(w[C::A - k] + w[C::A + k], w[C::A + 1 - k] + w[C::A + 1 + k]);
+                    zh = make_float2(w[C::A + 2 - k] + w[C::A + 2 + k], w[C::A + 3 - k] + w[C::A + 3 + k]);
+                }
+                sl = add2(add2(lo2(xm), lo2(xp)), zl);
+                sh = add2(add2(hi2(xm), hi2(xp)), zh);
+            } else if constexpr (kLap == 2) {
                 // full difference form: every neighbour minus the centre first
                 const float2 zl = make_float2((w[C::A - k] - cl.x) + (w[C::A + k] - cl.x),
                                               (w[C::A + 1 - k] - cl.y) + (w[C::A + 1 + k] - cl.y));
@@ -221,6 +317,15 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
         acc[i][0] = fma2(c1, dl, al);
         acc[i][1] = fma2(c1, dh, ah);
     }
+    if constexpr (YW > 0) {  // + P_y of this output plane (pencil warp)
+        static_assert(R1 == 1, "pencil variants run one row per consumer thread");
+        mbar_wait(yr.full + 8 * yr.st, yr.ph);
+        const float4 sy = *reinterpret_cast<const float4*>(yr.col + yr.st * (T1 * kT2));
+        mbar_arrive(yr.empty + 8 * yr.st);
+        ring_next<SS>(yr.st, yr.ph);
+        acc[0][0] = add2(acc[0][0], lo2(sy));
+        acc[0][1] = add2(acc[0][1], hi2(sy));
+    }
     // ---- aux tiles: u[t-1], m, damp ----
     mbar_wait(full_a + 8 * sa, pa_);
     const float* aux = acol + sa * (3 * C::ATILE / 4);
@@ -267,7 +372,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     epilogue_store<H, R1>(out, p, xoff, it, mine, un, lo_peer, hi_peer, g, K, c, pr);
 }
 
-template <int H, int R1, int T1, int SU, int SA, int U>
+template <int H, int R1, int T1, int SU, int SA, int U, int YW, int SS>
 struct Unrolled {
     __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + 1], int jb, Item& it,
                                                const float* ucol, const float* acol,
@@ -276,28 +381,28 @@ struct Unrolled {
                                                unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
                                                unsigned& mine, float* un, float* lo_peer,
                                                float* hi_peer, const Geo& g, const Coef& K,
-                                               const Ctl& c, const Peer& pr) {
+                                               const Ctl& c, const Peer& pr, YRing& yr) {
         if (jb + U < it.nq) {
-            consumer_step<H, R1, T1, SU, SA, 2 * H + 1, U>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
+            consumer_step<H, R1, T1, SU, SA, 2 * H + 1, U, YW, SS>(Q, jb + U, it, ucol, acol, aflag, full_u, empty_u,
                                                 full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                lo_peer, hi_peer, g, K, c, pr);
-            Unrolled<H, R1, T1, SU, SA, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                                                lo_peer, hi_peer, g, K, c, pr, yr);
+            Unrolled<H, R1, T1, SU, SA, U + 1, YW, SS>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                     full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                    lo_peer, hi_peer, g, K, c, pr);
+                                                    lo_peer, hi_peer, g, K, c, pr, yr);
         }
     }
 };
-template <int H, int R1, int T1, int SU, int SA>
-struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1> {
+template <int H, int R1, int T1, int SU, int SA, int YW, int SS>
+struct Unrolled<H, R1, T1, SU, SA, 2 * H + 1, YW, SS> {
     __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + 1], int, Item&,
                                                const float*, const float*, const unsigned*, unsigned,
                                                unsigned, unsigned, unsigned, unsigned&, unsigned&,
                                                unsigned&, unsigned&, unsigned&, unsigned&, float*,
                                                float*, float*, const Geo&, const Coef&, const Ctl&,
-                                               const Peer&) {}
+                                               const Peer&, YRing&) {}
 };
 
-template <int H, int R1, int T1, int SU, int SA, int UNR, int U>
+template <int H, int R1, int T1, int SU, int SA, int UNR, int U, int YW, int SS>
 struct ShiftBlock {
     __device__ __forceinline__ static void run(float4 (&Q)[R1][2 * H + UNR], int jb, Item& it,
                                                const float* ucol, const float* acol,
@@ -306,31 +411,32 @@ struct ShiftBlock {
                                                unsigned& pu, unsigned& sp, unsigned& sa, unsigned& pa_,
                                                unsigned& mine, float* un, float* lo_peer,
                                                float* hi_peer, const Geo& g, const Coef& K,
-                                               const Ctl& c, const Peer& pr) {
+                                               const Ctl& c, const Peer& pr, YRing& yr) {
         if (jb + U < it.nq) {
-            consumer_step<H, R1, T1, SU, SA, 2 * H + UNR, 2 * H + U>(
+            consumer_step<H, R1, T1, SU, SA, 2 * H + UNR, 2 * H + U, YW, SS>(
                 Q, jb + U, it, ucol, acol, aflag, full_u, empty_u, full_a, empty_a, su, pu, sp, sa, pa_,
-                mine, un, lo_peer, hi_peer, g, K, c, pr);
-            ShiftBlock<H, R1, T1, SU, SA, UNR, U + 1>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                mine, un, lo_peer, hi_peer, g, K, c, pr, yr);
+            ShiftBlock<H, R1, T1, SU, SA, UNR, U + 1, YW, SS>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                            full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                           lo_peer, hi_peer, g, K, c, pr);
+                                                           lo_peer, hi_peer, g, K, c, pr, yr);
         }
     }
 };
-template <int H, int R1, int T1, int SU, int SA, int UNR>
-struct ShiftBlock<H, R1, T1, SU, SA, UNR, UNR> {
+template <int H, int R1, int T1, int SU, int SA, int UNR, int YW, int SS>
+struct ShiftBlock<H, R1, T1, SU, SA, UNR, UNR, YW, SS> {
     __device__ __forceinline__ static void run(float4 (&)[R1][2 * H + UNR], int, Item&, const float*,
                                                const float*, const unsigned*, unsigned, unsigned, unsigned,
                                                unsigned, unsigned&, unsigned&, unsigned&, unsigned&,
                                                unsigned&, unsigned&, float*, float*, float*, const Geo&,
-                                               const Coef&, const Ctl&, const Peer&) {}
+                                               const Coef&, const Ctl&, const Peer&, YRing&) {}
 };
 
 // The kernel body: one time step over the items of this persistent CTA.
-template <int H, int R1, int T1, int SU, int SA, int UNR>
+template <int H, int R1, int T1, int SU, int SA, int UNR, int YW>
 __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const Coef& K, const Ctl& c,
                                          const Peer& pr, const Sched& sc) {
-    using C = Cfg<H, R1, T1>;
+    using C = Cfg<H, R1, T1, YW>;
+    constexpr int SS = YW > 0 ? 2 * YW : 1;  // y-pencil ring stages
     constexpr int NQ = C::NQ;
     // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
     // renaming; large halos: shift the queue (keeps the loop body small for the I-cache).
@@ -338,10 +444,13 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* uring = smem;
     unsigned char* aring = smem + SU * C::UPLANE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(aring + SA * 3 * C::ATILE);
-    unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA));  // damp-present per aux stage
+    float* sring = reinterpret_cast<float*>(aring + SA * 3 * C::ATILE);  // YW > 0: P_y stages (T1 x 64)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sring) +
+                                                 (YW > 0 ? SS * C::ATILE : 0));
+    unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA + SS));  // damp-present per aux stage
     const unsigned full_u = smem_addr(bars), empty_u = full_u + 8 * SU;
     const unsigned full_a = empty_u + 8 * SU, empty_a = full_a + 8 * SA;
+    const unsigned full_s = empty_a + 8 * SA, empty_s = full_s + 8 * SS;
     const unsigned uring_s = smem_addr(uring), aring_s = smem_addr(aring);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -354,14 +463,20 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             mbar_init(full_a + 8 * i, 1);
             mbar_init(empty_a + 8 * i, 32 * C::NCW);
         }
+        for (int i = 0; i < SS; ++i) {
+            mbar_init(full_s + 8 * i, 32);  // one pencil warp writes a stage
+            mbar_init(empty_s + 8 * i, 32 * C::NCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
     // per-CTA stamps (SWB_TRACE): [entry, after griddepcontrol.wait, warm-up done, consumers done,
     // exit] of the last two launches (even / odd step)
-    unsigned long long* tr = c.trace ? c.trace + 8 * (blockIdx.x + 1024 * (c.step & 1)) : nullptr;
-    if (tr && threadIdx.x == 0) tr[0] = gtimer();
+    // (recomputed from the launch parameters at each use: a pointer kept live would cost the
+    // register-capped variants a spill)
+#define SWB_TRACE_AT(i) c.trace[8 * blockIdx.x + (i)]  // (the host offsets c.trace by the step parity)
+    if (c.trace && threadIdx.x == 0) SWB_TRACE_AT(0) = gtimer();
     // Programmatic dependent launch: everything above overlapped the previous step's tail;
     // u[t], u[t-1] written by that step are only touched after this point.
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -370,7 +485,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     const int nitems = sc.ncol * sc.nchunk;
     const int first = static_cast<int>(blockIdx.x), G = static_cast<int>(gridDim.x);  // persistent CTAs
     unsigned mine = 0u;
-    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+    if (c.trace && threadIdx.x == 0) SWB_TRACE_AT(1) = gtimer();
 
     if (warp == 0) {
         // ===== TMA producers: lane 0 feeds the u ring, lane 1 the aux ring, each limited
@@ -438,6 +553,11 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                 }
             }
         }
+    } else if (YW > 0 && warp > C::NCW) {
+        // ===== y-pencil warps =====
+        if constexpr (YW > 0)
+            ypencil_loop<H, T1, SU, SS, YW>(warp - C::NCW - 1, lane, uring, sring, full_u, full_s, empty_s, K,
+                                            sc, first, G, nitems);
     } else {
         // ===== consumers =====
         const int ct = threadIdx.x - 32;
@@ -453,6 +573,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
         float4 Q[R1][kUnroll ? NQ : 1];              // rotating register queue (H <= SWB_UNROLL_MAXH)
         float4 Qs[R1][kUnroll ? 1 : 2 * H + UNR];   // shifting register queue
         unsigned su = 0, pu = 0, sp = 0, sa = 0, pa_ = 0;
+        YRing yr{full_s, empty_s, sring + r0 * kT2 + 4 * tz, 0u, 0u};
         for (int item = first; item < nitems; item += G) {
             const int col = item % sc.ncol, chunk = item / sc.ncol;
             Item it;
@@ -489,27 +610,27 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             it.gcol = static_cast<long long>(it.yt) * g.P2 + it.zc;
             it.xrun = static_cast<long long>(it.q0 + it.dir * H) * g.plane + it.gcol;  // first output plane
             sp = (su + H) % SU;  // stage of plane j = H, the first output plane of this item
-            if (tr && ct == 0 && item == first) {
+            if (c.trace && ct == 0 && item == first) {
                 // time when the first output plane's data is complete (end of warm-up)
                 unsigned s2 = (su + 2 * H) % SU, p2 = pu ^ (((su + 2 * H) / SU) & 1u);
                 mbar_wait(full_u + 8 * s2, p2);
-                tr[2] = gtimer();
+                SWB_TRACE_AT(2) = gtimer();
             }
             if constexpr (kUnroll) {
 #pragma unroll 1
                 for (int jb = 0; jb < it.nq; jb += NQ)
-                    Unrolled<H, R1, T1, SU, SA, 0>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
+                    Unrolled<H, R1, T1, SU, SA, 0, YW, SS>::run(Q, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                         full_a, empty_a, su, pu, sp, sa, pa_, mine,
-                                                        un, lo_peer, hi_peer, g, K, c, pr);
+                                                        un, lo_peer, hi_peer, g, K, c, pr, yr);
             } else {
                 // Partial unroll by UNR with a queue of 2H+UNR slots: plane j-m lives in slot
                 // 2H+u-m inside a block, and the queue shifts down by UNR once per block
                 // (2H/UNR float4 moves per plane instead of 2H).
 #pragma unroll 1
                 for (int jb = 0; jb < it.nq; jb += UNR) {
-                    ShiftBlock<H, R1, T1, SU, SA, UNR, 0>::run(Qs, jb, it, ucol, acol, aflag, full_u, empty_u,
+                    ShiftBlock<H, R1, T1, SU, SA, UNR, 0, YW, SS>::run(Qs, jb, it, ucol, acol, aflag, full_u, empty_u,
                                                              full_a, empty_a, su, pu, sp, sa, pa_, mine, un,
-                                                             lo_peer, hi_peer, g, K, c, pr);
+                                                             lo_peer, hi_peer, g, K, c, pr, yr);
 #pragma unroll
                     for (int i = 0; i < R1; ++i)
 #pragma unroll
@@ -522,55 +643,60 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     // (peer stores reach system scope through thread 0's __threadfence_system in
     // signal_neighbours, after the CTA barrier in block_max_commit: fence cumulativity)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (tr && threadIdx.x == 32) tr[3] = gtimer();
+    if (c.trace && threadIdx.x == 32) SWB_TRACE_AT(3) = gtimer();
     block_max_commit(mine, c.smax + c.slot);  // (contains the CTA barrier)
     signal_neighbours(c);
-    if (tr && threadIdx.x == 0) tr[4] = gtimer();
+    if (c.trace && threadIdx.x == 0) SWB_TRACE_AT(4) = gtimer();
+#undef SWB_TRACE_AT
 }
 
-template <int H, int R1, int T1, int SU, int SA, int UNR>
-__global__ void __launch_bounds__(Cfg<H, R1, T1>::NTHREADS, 1)
+template <int H, int R1, int T1, int SU, int SA, int UNR, int YW>
+__global__ void __launch_bounds__(Cfg<H, R1, T1, YW>::NTHREADS, 1)
     k_tma(const __grid_constant__ Maps maps, Geo g, Coef K, Ctl c, Peer pr, Sched sc) {
-    tma_body<H, R1, T1, SU, SA, UNR>(maps, g, K, c, pr, sc);
+    tma_body<H, R1, T1, SU, SA, UNR, YW>(maps, g, K, c, pr, sc);
 }
-template <int H, int R1, int T1, int SU, int SA>
+template <int H, int R1, int T1, int SU, int SA, int YW>
 size_t smem_bytes() {
-    using C = Cfg<H, R1, T1>;
-    return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE + 16 * (SU + SA) + 4 * SA;
+    using C = Cfg<H, R1, T1, YW>;
+    constexpr int SS = YW > 0 ? 2 * YW : 1;
+    return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
+           (YW > 0 ? static_cast<size_t>(SS) * C::ATILE : 0) + 16 * (SU + SA + SS) + 4 * SA;
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
-// (H, R1, T1, SU, SA, UNR): rows per thread, tile rows, u-ring stages, aux-ring stages,
-// queue unroll (ignored for H <= 3, which rotates the queue by renaming).
+// (H, R1, T1, SU, SA, UNR, YW): rows per thread, tile rows, u-ring stages, aux-ring stages,
+// queue unroll (ignored for H <= 4, which rotates the queue by renaming), y-pencil warps.
 #define SWB_TMA_VARIANTS(X)      \
-    X(1, 1, 30, 5, 4, 1)         \
-    X(2, 1, 30, 6, 4, 1)         \
-    X(3, 1, 30, 7, 4, 1)         \
-    X(4, 1, 30, 8, 4, 4)         \
-    X(5, 1, 30, 10, 4, 2)        \
-    X(6, 1, 30, 10, 3, 2)        \
-    X(7, 1, 22, 14, 3, 2)        \
-    X(8, 1, 22, 11, 3, 4)        \
-    X(1, 1, 28, 5, 4, 1)         \
-    X(2, 1, 28, 6, 4, 1)         \
-    X(3, 1, 28, 7, 4, 1)         \
-    X(4, 1, 28, 8, 4, 4)         \
-    X(5, 1, 28, 10, 4, 2)        \
-    X(6, 1, 28, 10, 3, 4)        \
-    X(8, 1, 20, 11, 3, 4)
+    X(1, 1, 30, 5, 4, 1, 0)         \
+    X(2, 1, 30, 6, 4, 1, 0)         \
+    X(3, 1, 30, 7, 4, 1, 0)         \
+    X(4, 1, 30, 8, 4, 4, 0)         \
+    X(5, 1, 30, 10, 4, 2, 0)        \
+    X(6, 1, 30, 10, 3, 2, 0)        \
+    X(7, 1, 22, 14, 3, 2, 0)        \
+    X(8, 1, 22, 11, 3, 4, 0)        \
+    X(1, 1, 28, 5, 4, 1, 0)         \
+    X(2, 1, 28, 6, 4, 1, 0)         \
+    X(3, 1, 28, 7, 4, 1, 0)         \
+    X(4, 1, 28, 8, 4, 4, 0)         \
+    X(5, 1, 28, 10, 4, 2, 0)        \
+    X(6, 1, 28, 10, 3, 4, 0)        \
+    X(8, 1, 20, 11, 3, 4, 0)        \
+    X(8, 1, 20, 11, 3, 4, 1)
+
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
 
 struct Variant {
-    int H, R1, T1, SU, SA, UNR;
+    int H, R1, T1, SU, SA, UNR, YW;
     KernelFn fn;
     size_t smem;
     int threads;
 };
 
-#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa, unr)                                        \
-    {h, r1, t1, su, sa, unr, k_tma<h, r1, t1, su, sa, unr>, smem_bytes<h, r1, t1, su, sa>(), \
-     Cfg<h, r1, t1>::NTHREADS},
+#define SWB_VARIANT_ENTRY(h, r1, t1, su, sa, unr, yw)                                              \
+    {h, r1, t1, su, sa, unr, yw, k_tma<h, r1, t1, su, sa, unr, yw>, smem_bytes<h, r1, t1, su, sa, yw>(), \
+     Cfg<h, r1, t1, yw>::NTHREADS},
 
 // Rows per consumer thread: R1 = 1 doubles the consumer warps per SM (more latency hiding)
 // at the cost of re-reading the y-neighbour rows per row; SWB_R1=1|2 overrides the default.
@@ -603,30 +729,46 @@ int preferred_t1(int H) {
     return 0;  // 0: first matching variant
 }
 
-// t1_want: tile height chosen by tma_plan (0: any); SWB_T1 overrides it.
-const Variant* find_variant(int H, int t1_want = 0) {
+// y-pencil warps per CTA (0: the consumers read the 2H y neighbours themselves); SWB_YW overrides.
+int preferred_yw(int H) {
+    const char* env = std::getenv("SWB_YW");
+    if (env && env[0] >= '0' && env[0] <= '9') return env[0] - '0';
+    (void)H;
+    return -1;  // -1: the plan's choice
+}
+
+// t1_want / yw_want: tile height and pencil warps chosen by tma_plan (0: any height / none);
+// SWB_T1 and SWB_YW override them.
+const Variant* find_variant(int H, int t1_want = 0, int yw_want = 0) {
     static const Variant table[] = {SWB_TMA_VARIANTS(SWB_VARIANT_ENTRY)};
     const int r1 = preferred_r1(H), unr = preferred_unr(H), su = preferred_su(H);
     const int t1 = preferred_t1(H) ? preferred_t1(H) : t1_want;
-    for (const auto& v : table)
-        if (v.H == H && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su) && (t1 == 0 || v.T1 == t1)) return &v;
-    for (const auto& v : table)
-        if (v.H == H && v.R1 == r1 && (unr == 0 || v.UNR == unr) && (t1 == 0 || v.T1 == t1)) return &v;
-    for (const auto& v : table)
-        if (v.H == H && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su)) return &v;
-    for (const auto& v : table)
-        if (v.H == H && v.R1 == r1 && v.UNR == unr) return &v;
-    for (const auto& v : table)
-        if (v.H == H && v.R1 == r1) return &v;
-    for (const auto& v : table)
-        if (v.H == H) return &v;
+    const int yw_pref = preferred_yw(H) >= 0 ? preferred_yw(H) : yw_want;
+    for (int yw : {yw_pref, 0}) {
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su) &&
+                (t1 == 0 || v.T1 == t1))
+                return &v;
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw && v.R1 == r1 && (unr == 0 || v.UNR == unr) && (t1 == 0 || v.T1 == t1))
+                return &v;
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw && v.R1 == r1 && v.UNR == unr && (su == 0 || v.SU == su)) return &v;
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw && v.R1 == r1 && v.UNR == unr) return &v;
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw && v.R1 == r1) return &v;
+        for (const auto& v : table)
+            if (v.H == H && v.YW == yw) return &v;
+    }
     return nullptr;
 }
 
-// A variant with exactly this tile height exists for the halo (rows-per-thread preference applied).
-bool find_variant_exact_t1(int H, int t1) {
-    const Variant* v = find_variant(H, t1);
-    return v && v->T1 == t1;
+// A variant with exactly this tile height and pencil count exists for the halo (rows-per-thread
+// preference applied).
+bool find_variant_exact(int H, int t1, int yw) {
+    const Variant* v = find_variant(H, t1, yw);
+    return v && v->T1 == t1 && v->YW == yw;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -675,7 +817,9 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // latency bound, not proportional to rows).  At 256^3 SO 16 this picks 20 rows: 48 columns x 3
     // chunks fill 144 of 148 SMs instead of 132 (+2.4 %); at 512^3 it keeps 22 (20 rows: -8 %).
     // Ties go to the height that wastes fewer interior rows.  SWB_TPLAN=rows: row efficiency only
-    // (the previous rule, development A/B).
+    // (the previous rule, development A/B).  A variant with a y-pencil warp streams a plane in
+    // kPencilTime of the time (SO 16, 20 rows: 219.4 against 208.5 GPts/s at 256^3; at 512^3 the
+    // 22-row tile without it stays ahead, 250 against 240).
     const int rows = g.y1 - g.y0;
     const int np_all = g.x1 - g.x0;
     const int zs_all = g.z0 & ~3;
@@ -696,23 +840,29 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         if (nchunk_out) *nchunk_out = best_nc;
         return best_cost * std::pow(static_cast<double>(t1), 0.25);
     };
-    int t1_best = 0;
+    constexpr double kPencilTime = 0.95;
+    int t1_best = 0, yw_best = 0;
     double eff_best = -1.0, cost_best = 1e300;
-    for (int cand : {30, 28, 22, 20}) {
-        if ((H <= 6) != (cand >= 28)) continue;
-        if (!find_variant_exact_t1(H, cand)) continue;
-        const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
-        const double cost = rows_only || np_all <= 0 || rows <= 0 ? 0.0 : makespan(cand, nullptr);
-        if (cost < cost_best * (1 - 1e-9) || (cost <= cost_best * (1 + 1e-9) && eff > eff_best + 1e-9)) {
-            cost_best = cost;
-            eff_best = eff;
-            t1_best = cand;
+    for (int yw : {0, 1})
+        for (int cand : {30, 28, 22, 20}) {
+            if ((H <= 6) != (cand >= 28)) continue;
+            if (!find_variant_exact(H, cand, yw)) continue;
+            const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
+            const double cost = rows_only || np_all <= 0 || rows <= 0
+                                    ? 0.0
+                                    : makespan(cand, nullptr) * (yw ? kPencilTime : 1.0);
+            if (cost < cost_best * (1 - 1e-9) || (cost <= cost_best * (1 + 1e-9) && eff > eff_best + 1e-9)) {
+                cost_best = cost;
+                eff_best = eff;
+                t1_best = cand;
+                yw_best = yw;
+            }
         }
-    }
-    const Variant* v = find_variant(H, t1_best);
+    const Variant* v = find_variant(H, t1_best, yw_best);
     if (!v) return p;
-    p.variant = 1000 + 100 * (v->R1 - 1) + 10 * v->UNR + H + 100000 * v->T1;
+    p.variant = 1000 + 100 * (v->R1 - 1) + 10 * v->UNR + H + 100000 * v->T1 + 10000000 * v->YW;
     p.T1 = v->T1;
+    p.yw = v->YW;
     p.T2 = kT2;
     p.A = (H + 3) / 4 * 4;
     p.threads = v->threads;
@@ -876,7 +1026,7 @@ void tma_damp_flags(const TmaPlan& plan, const Geo& g, const float* damp, int n1
 
 cudaError_t launch_tma(const TmaPlan& plan, const void* maps, const Geo& g, const Coef& K,
                        const Ctl& c, const Peer& p, cudaStream_t s) {
-    const Variant* v = find_variant(plan.H, plan.T1);
+    const Variant* v = find_variant(plan.H, plan.T1, plan.yw);
     if (!plan.ok || !v) return cudaErrorInvalidValue;
     Sched sc;
     sc.nyt = plan.tiles_y;

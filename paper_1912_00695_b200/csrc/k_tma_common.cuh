@@ -93,7 +93,7 @@ __device__ __forceinline__ void set_comp(float4& v, int e, float x) {
     else v.w = x;
 }
 
-template <int H, int R1, int T1>
+template <int H, int R1, int T1, int YW = 0>
 struct Cfg {
     static constexpr int A = (H + 3) / 4 * 4;         // dim-2 halo rounded to float4
     static constexpr int W2 = kT2 + 2 * A;             // smem row length (floats)
@@ -101,7 +101,7 @@ struct Cfg {
     static constexpr int UPLANE = (ROWS * W2 * 4 + 127) / 128 * 128;
     static constexpr int ATILE = T1 * kT2 * 4;         // one aux tile (bytes)
     static constexpr int NCW = (T1 / R1) * 16 / 32;    // consumer warps
-    static constexpr int NTHREADS = 32 * (NCW + 1);
+    static constexpr int NTHREADS = 32 * (NCW + 1 + YW);  // + YW y-pencil warps (k_tma.cu)
     static constexpr int NQ = 2 * H + 1;               // queue depth
 };
 

@@ -26,6 +26,7 @@ struct TmaPlan {
     int ok;
     int H;
     int T1, T2;           // output tile rows (dim 1) and cols (dim 2)
+    int yw;               // y-pencil warps of the variant (0 or 1)
     int A;                // dim-2 halo rounded up to a multiple of 4
     int stages;           // u-plane ring depth
     int threads;

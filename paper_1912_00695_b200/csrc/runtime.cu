@@ -328,6 +328,7 @@ int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
         Ctl c = h->ctl;
         c.step = s;
         c.slot = slot0 + i;
+        if (c.trace) c.trace += static_cast<size_t>(s & 1) * 8 * 1024;  // SWB_TRACE: even / odd step
         c.err = h->d_err;
         c.ghost_lo_end = 0;
         c.ghost_hi_begin = INT_MAX;
