@@ -4,9 +4,9 @@
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck synccheck racecheck initcheck; do
-  cases="k1 simple slabs extras"
+  cases=${CASES:-"k1 pencil simple slabs extras"}
   # initcheck serialises co-resident grids: the fused-ordering slabs would hit their 20 s bounded wait
-  [ $tool = initcheck ] && cases="k1 simple slabs_ordered extras"
+  [ $tool = initcheck ] && cases=${CASES_INIT:-"k1 pencil_single simple slabs_ordered extras"}
   for case in $cases; do
     timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 python scripts/sanitize_cases.py $case \
         > gpurun_out/sanitize_${tool}_${case}.log 2>&1

@@ -1,5 +1,5 @@
 """Small workloads for compute-sanitizer (scripts/sanitize.sh): every kernel family on grids
-small enough for the tools' instrumentation -- K1 (TMA 2.5D) at SO 2/4/8/12/16 with damping,
+small enough for the tools' instrumentation -- K1 (TMA 2.5D) at SO 2/4/8/12/16 with damping, the SO 16 y-pencil variant,
 source and receivers, the plain FP64/FP32 and factorised one-thread-per-point kernels, z-slabs
 with the kernel-ordered exchange and with the fused in-kernel ordering (grid capped so both
 persistent grids are co-resident on one GPU), snapshots and the adjoint.
@@ -52,6 +52,25 @@ def slabs(modes=(False, True)):
     os.environ.pop("SWB_MAX_CTAS", None)
 
 
+def pencil(fused=True):
+    """K1 with the y-pencil warp (SO 16, 20-row tile, forced), single domain and fused slabs."""
+    os.environ["SWB_YW"], os.environ["SWB_T1"] = "1", "20"
+    pr = prob((40, 50, 70), 16, 5)
+    rec = np.array([[20, 25, z] for z in range(8, 60, 5)], np.int32)
+    P.run(pr, receivers=rec)
+    if fused:
+        os.environ["SWB_FUSED_SAME_DEVICE"], os.environ["SWB_MAX_CTAS"] = "1", "60"
+        ops = [P.Operator(pr, slab=s) for s in ((0, 20), (20, 40))]
+        P.Operator.link_local(ops[0], ops[1])
+        for o in ops:
+            o.apply_async(5, 0)
+        for o in ops:
+            o.collect(5)
+            o.close()
+    for k in ("SWB_YW", "SWB_T1", "SWB_FUSED_SAME_DEVICE", "SWB_MAX_CTAS"):
+        os.environ.pop(k, None)
+
+
 def extras():
     pr = prob((30, 32, 70), 8, 8)
     rec = np.array([[15, 16, z] for z in range(4, 60, 5)], np.int32)
@@ -77,7 +96,7 @@ def slabs_ordered():
         o.close()
 
 
-CASES = {"k1": k1, "simple": simple, "slabs": slabs, "slabs_ordered": slabs_ordered, "extras": extras}
+CASES = {"k1": k1, "pencil": pencil, "pencil_single": lambda: pencil(False), "simple": simple, "slabs": slabs, "slabs_ordered": slabs_ordered, "extras": extras}
 if __name__ == "__main__":
     for name in sys.argv[1:] or list(CASES):
         CASES[name]()
