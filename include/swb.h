@@ -51,7 +51,8 @@ extern "C" {
  * SWB_FORM_FACTORISED : aggressive algebra, FP32 Laplacian (difference form on the k=1 ring).
  *                       The production kernel (TMA 2.5D, isotropic spacing, SO >= 2) combines in
  *                       FP32 with per-point coefficient fields B = 1/(m+g), A = (m-g)/(m+g),
- *                       g = damp dt/2 (computed once per handle in FP64, rounded once):
+ *                       g = damp dt/2 (computed once per handle in FP64, rounded once to a
+ *                       neighbouring float chosen by a hash of the cell: unbiased):
  *                       u+ = u + A (u - u-) + B Lr (dt/h)^2.  Anisotropic spacing takes the
  *                       one-thread-per-point fallback with an FP64 final combine.
  * SWB_FORM_PLAIN_F64  : basic form evaluated exactly as the interpreter does (double,
