@@ -436,7 +436,7 @@ template <int H, int R1, int T1, int SU, int SA, int UNR, int YW>
 __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const Coef& K, const Ctl& c,
                                          const Peer& pr, const Sched& sc) {
     using C = Cfg<H, R1, T1, YW>;
-    constexpr int SS = YW > 0 ? 2 * YW : 1;  // y-pencil ring stages
+    constexpr int SS = YW > 0 ? 2 * YW : 1;  // y-pencil ring stages (4 measured equal)
     constexpr int NQ = C::NQ;
     // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
     // renaming; large halos: shift the queue (keeps the loop body small for the I-cache).
@@ -682,7 +682,7 @@ size_t smem_bytes() {
     X(5, 1, 28, 10, 4, 2, 0)        \
     X(6, 1, 28, 10, 3, 4, 0)        \
     X(8, 1, 20, 11, 3, 4, 0)        \
-    X(8, 1, 20, 11, 3, 4, 1)
+    X(8, 1, 20, 13, 3, 4, 1)
 
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
