@@ -138,6 +138,8 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
 // FFMA2 chains are the bound) against the consumers; measured at SO 16 on B200 (256^3, 20-row tile,
 // GPts/s): kP = 3: 202, 4: 209, 5: 219, 6: 214, 7: 209, 8: 201, no pencil 208.5
 // (profiles/pencil_r02.txt).
+// (SO 8 and SO 12 variants with a pencil warp, 16 warps at 128 registers, measured slower:
+// SO 8 k >= 3: 307 -> 302, k >= 2: 281; SO 12 k >= 4: 251 -> 247, k >= 5: 242 GPts/s at 256^3)
 template <int H>
 constexpr int pencil_k() { return H - 3; }
 
