@@ -231,7 +231,7 @@ const char* swb_version(void);
 
 /* Debug: with SWB_TRACE=1 in the environment at swb_create, copy the per-CTA globaltimer
  * stamps of the last K1 launch of an even and of an odd step: out[parity][cta][8] =
- * {entry, after griddepcontrol.wait, warm-up done, compute done, exit, 0, 0, 0}
+ * {entry, after griddepcontrol.wait, warm-up done, compute done, exit, SM id, 0, 0}
  * (out holds 2 * 8 * max_ctas values).  Returns the number of CTAs (or a negative error). */
 int swb_debug_trace(swb_handle* h, unsigned long long* out, int max_ctas);
 

@@ -478,7 +478,12 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     // (recomputed from the launch parameters at each use: a pointer kept live would cost the
     // register-capped variants a spill)
 #define SWB_TRACE_AT(i) c.trace[8 * blockIdx.x + (i)]  // (the host offsets c.trace by the step parity)
-    if (c.trace && threadIdx.x == 0) SWB_TRACE_AT(0) = gtimer();
+    if (c.trace && threadIdx.x == 0) {
+        SWB_TRACE_AT(0) = gtimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        SWB_TRACE_AT(5) = smid;
+    }
     // Programmatic dependent launch: everything above overlapped the previous step's tail;
     // u[t], u[t-1] written by that step are only touched after this point.
     asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -39,3 +39,18 @@ print(f"  stream time per CTA (wait done -> compute done) med {np.median(busy):.
       f"max {busy.max():.2f}; SM-time busy fraction over the period "
       f"{busy.sum() / (148 * (a[1, :, 1].min() - a[0, :, 1].min())):.3f}")
 op.close()
+# per-CTA detail of step t: stream time against the SM id and the item (column, chunk)
+raw = np.array(buf[:], dtype=np.float64).reshape(2, 1024, 8)[0, :g]
+sm = raw[:, 5].astype(int)
+st = (raw[:, 3] - raw[:, 1]) / 1e3
+if os.environ.get("TRACE_DETAIL"):
+    order = np.argsort(st)
+    print("  fastest 6 (cta, sm, us):", [(int(b), int(sm[b]), round(float(st[b]), 2)) for b in order[:6]])
+    print("  slowest 6 (cta, sm, us):", [(int(b), int(sm[b]), round(float(st[b]), 2)) for b in order[-6:]])
+    for name, key in (("sm // 2 (TPC) parity", lambda b: (sm[b] // 2) % 2), ("sm < 74", lambda b: int(sm[b] < 74)),
+                      ("sm % 4", lambda b: sm[b] % 4)):
+        grp = {}
+        for b in range(g):
+            grp.setdefault(key(b), []).append(st[b])
+        print(f"  by {name}: " + "  ".join(f"{k}:{np.mean(v):.2f}" for k, v in sorted(grp.items())))
+    np.save("gpurun_out/trace_detail_%d_%d.npy" % (so, n), raw)
