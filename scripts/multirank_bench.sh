@@ -5,7 +5,7 @@
 mkdir -p gpurun_out
 for n in 2 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-      --master-port $((29600 + n)) bench.py --gpus $n --steps 100 --warmup 5 --sweep-steps 50 --e2e-reps 2 \
+      --master-port $((29600 + n)) bench.py --gpus $n --allow-shared-gpu --steps 100 --warmup 5 --sweep-steps 50 --e2e-reps 2 \
       > gpurun_out/mr_bench_$n.json 2> gpurun_out/mr_bench_$n.err
   echo "ours N=$n rc=$?"; tail -c 1500 gpurun_out/mr_bench_$n.json; echo
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
