@@ -41,6 +41,9 @@ namespace swb {
 namespace {
 using namespace tma;
 
+#ifndef SWB_DIFF_K
+#define SWB_DIFF_K 1  // difference form (neighbour minus centre) for the terms k <= SWB_DIFF_K
+#endif
 #ifndef SWB_UNROLL_MAXH
 #define SWB_UNROLL_MAXH 4  // rotate the register queue by renaming up to this halo (measured: +1 % at SO 8; I-cache misses beyond)
 #endif
@@ -265,7 +268,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
                 }
                 sl = add2(add2(lo2(xm), lo2(xp)), zl);
                 sh = add2(add2(hi2(xm), hi2(xp)), zh);
-            } else if constexpr (kLap == 2) {
+            } else if (kLap == 2 || k <= SWB_DIFF_K) {
                 // full difference form: every neighbour minus the centre first
                 const float2 zl = make_float2((w[C::A - k] - cl.x) + (w[C::A + k] - cl.x),
                                               (w[C::A + 1 - k] - cl.y) + (w[C::A + 1 + k] - cl.y));
@@ -345,7 +348,8 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     ring_next<SA>(sa, pa_);
     if (++sp == SU) sp = 0;
     // ---- combine: u+ = u + A (u - u-) + B Lr (dt/h)^2 (coefficient fields, tma_update_coefs) ----
-    const float2 R3 = splat(lap_form<H>() == 2 ? K.R3f : K.R3), khi = splat(K.kap_hi), klo = splat(K.kap_lo);
+    const float2 R3 = splat(lap_form<H>() == 2 ? K.R3f : (SWB_DIFF_K > 1 ? K.R3k[SWB_DIFF_K - 1] : K.R3)),
+                 khi = splat(K.kap_hi), klo = splat(K.kap_lo);
     float4 out[R1];
 #pragma unroll
     for (int i = 0; i < R1; ++i) {

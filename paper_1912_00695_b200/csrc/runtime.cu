@@ -268,6 +268,11 @@ void coef_from(const swb_problem* p, int H, const float* w, Coef& K) {
         double r = c0;
         for (int k = 1; k <= H; ++k) r += 2.0 * static_cast<double>(K.c[k]);
         K.R3f = static_cast<float>(3.0 * r);
+        double rd = c0;
+        for (int d = 0; d < 4; ++d) {
+            if (d + 1 <= H) rd += 2.0 * static_cast<double>(K.c[d + 1]);
+            K.R3k[d] = static_cast<float>(3.0 * rd);
+        }
     }
     const double h0 = static_cast<double>(p->spacing[0]);
     const double kap = (dt / h0) * (dt / h0);

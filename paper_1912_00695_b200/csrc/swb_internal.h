@@ -41,6 +41,7 @@ struct Coef {
     double inject;          // double(dt) * double(dt)   (source scale numerator)
     float R3;               // fp32(3 (c0 + 2 c1))  (isotropic residual)
     float R3f;              // fp32(3 (c0 + 2 sum_k>=1 c_k)) in double: residual of the full difference form
+    float R3k[4];           // fp32(3 (c0 + 2 sum_{k<=d+1} c_k)): residual with the difference form for k <= d+1
     float kap_hi, kap_lo;   // (dt/h)^2 as an exact-ish float pair (isotropic)
     float half_dt;          // dt/2 (exact)
     int iso;                // h[0]==h[1]==h[2]
