@@ -19,13 +19,14 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     device = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     form = sys.argv[1] if len(sys.argv) > 1 else "factorised"
-    shape, so, nt = (40, 24, 26), 8, 17
+    so = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    shape, nt = ((40, 24, 26) if so <= 8 else (60, 30, 40)), 17
     rng = np.random.default_rng(11)
     vel = (1500 + 1000 * rng.random(shape)).astype(np.float32)
     prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
                                                    steps=nt, velocity_field=vel, damp_max=0.05, damp_width=4,
                                                    source_point=[15, 12, 13]))
-    rec = np.array([[x, 12, 13] for x in range(shape[0])], np.int32)
+    rec = np.array([[x, 12, 13] for x in range(shape[0])], np.int32)  # (on-grid line through the slabs)
     slab = D.slab_bounds(shape[0], world, rank)
     op = P.Operator(prob, form=form, device=device, slab=slab, receivers=rec)
     D.exchange_and_link(op, rank, world)

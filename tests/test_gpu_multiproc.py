@@ -20,3 +20,14 @@ def test_multiprocess_slabs_bitwise(world, form):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-4000:]
     assert "MP_SLAB_OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+def test_multiprocess_slabs_bitwise_so16_pencil():
+    """The SO 16 K1 variant with the y-pencil warp (forced) across two IPC-linked processes."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29571",
+           os.path.join(ROOT, "scripts", "mp_slab_check.py"), "factorised", "16"]
+    env = dict(os.environ, SWB_YW="1", SWB_T1="20")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-4000:]
+    assert "MP_SLAB_OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
