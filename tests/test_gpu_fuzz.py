@@ -2,6 +2,8 @@
 every even space order up to 16, damping widths, heterogeneous velocity, source and receivers
 anywhere in the interior, random initial levels, step counts that are odd and even.
 plain FP64 bit-exact (levels, per-step max, traces); factorised <= 1e-5; K3 == K1 bitwise."""
+import os
+
 import numpy as np
 import pytest
 
@@ -34,7 +36,7 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-@pytest.mark.parametrize("seed", range(64))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SWB_FUZZ_CASES", "64"))))
 def test_random_configuration(seed):
     so, shape, nt, vel, damp, width, src, rec, init = _case(seed)
     cfg = P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so, steps=nt,
