@@ -137,14 +137,27 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
 // Each lane owns one float4 column and half of the tile rows and holds its whole pencil (T1/2 + 2H
 // rows) in registers, so every u value is read from shared memory once per pencil instead of once
 // per output that needs it; P_y goes to a two-stage ring and the consumers read it with one
-// LDS.128 in place of 2 (H - kP + 1) loads.  kP balances the pencil warp (one warp per CTA, its
-// FFMA2 chains are the bound) against the consumers; measured at SO 16 on B200 (256^3, 20-row tile,
-// GPts/s): kP = 3: 202, 4: 209, 5: 219, 6: 214, 7: 209, 8: 201, no pencil 208.5
-// (profiles/pencil_r02.txt).
+// LDS.128 in place of 2 (H - kP + 1) loads.  kP balances the pencil warp against the consumers.
+// Warps are spread over the four SM sub-partitions as warp % 4, so the pencil warp shares an issue
+// port with whatever warps sit on its sub-partition: placed after the consumers (warp 11) it shared
+// one with two consumer warps and was issue-bound beyond kP = 5; placed at warp 4 it shares one with
+// the (nearly idle) TMA producer warp and one consumer, and takes one more y pair.  Measured at SO 16
+// on B200 (256^3, 20-row tile, GPts/s; profiles/pencil_r02.txt, pencil_place_r02.txt):
+//   warp 11: kP = 3: 202, 4: 209, 5: 219, 6: 214, 7: 209, 8: 201;   no pencil 208.5 / 209.5
+//   warp 4:  kP = 3: 227.9, 4: 230.6, 5: 225.6
 // (SO 8 and SO 12 variants with a pencil warp, 16 warps at 128 registers, measured slower:
 // SO 8 k >= 3: 307 -> 302, k >= 2: 281; SO 12 k >= 4: 251 -> 247, k >= 5: 242 GPts/s at 256^3)
+#ifndef SWB_PENCIL_K
+#define SWB_PENCIL_K 0  // development override of the pencil split point (0: H - 4)
+#endif
+#ifndef SWB_PENCIL_WARP
+#define SWB_PENCIL_WARP 4  // physical warp of the first pencil warp (0: after the consumers)
+#endif
+#ifndef SWB_PENCIL_SS
+#define SWB_PENCIL_SS 0  // development override of the P_y ring depth (0: 2 per pencil warp)
+#endif
 template <int H>
-constexpr int pencil_k() { return H - 3; }
+constexpr int pencil_k() { return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : H - 4; }
 
 struct YRing {
     unsigned full, empty;  // mbarriers of stage 0 (8 bytes apart)
@@ -442,7 +455,7 @@ template <int H, int R1, int T1, int SU, int SA, int UNR, int YW>
 __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const Coef& K, const Ctl& c,
                                          const Peer& pr, const Sched& sc) {
     using C = Cfg<H, R1, T1, YW>;
-    constexpr int SS = YW > 0 ? 2 * YW : 1;  // y-pencil ring stages (4 measured equal)
+    constexpr int SS = YW > 0 ? (SWB_PENCIL_SS > 0 ? SWB_PENCIL_SS : 2 * YW) : 1;  // y-pencil ring stages
     constexpr int NQ = C::NQ;
     // Small halos: unroll the plane loop by the queue depth so the register queue rotates by
     // renaming; large halos: shift the queue (keeps the loop body small for the I-cache).
@@ -460,6 +473,11 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     const unsigned uring_s = smem_addr(uring), aring_s = smem_addr(aring);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // roles: warp 0 producer; pencil warps PW0 .. PW0 + YW - 1; the other warps are consumers in
+    // order (warps are spread over the SM sub-partitions as warp % 4)
+    constexpr int PW0 = (YW > 0 && SWB_PENCIL_WARP > 0) ? SWB_PENCIL_WARP : C::NCW + 1;
+    const bool is_pencil = YW > 0 && warp >= PW0 && warp < PW0 + YW;
+    const int cw = warp - 1 - ((YW > 0 && warp >= PW0 + YW) ? YW : 0);  // consumer ordinal
     if (threadIdx.x == 0) {
         for (int i = 0; i < SU; ++i) {
             mbar_init(full_u + 8 * i, 1);
@@ -564,14 +582,14 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                 }
             }
         }
-    } else if (YW > 0 && warp > C::NCW) {
+    } else if (is_pencil) {
         // ===== y-pencil warps =====
         if constexpr (YW > 0)
-            ypencil_loop<H, T1, SU, SS, YW>(warp - C::NCW - 1, lane, uring, sring, full_u, full_s, empty_s, K,
+            ypencil_loop<H, T1, SU, SS, YW>(warp - PW0, lane, uring, sring, full_u, full_s, empty_s, K,
                                             sc, first, G, nitems);
     } else {
         // ===== consumers =====
-        const int ct = threadIdx.x - 32;
+        const int ct = cw * 32 + lane;
         const int tz = ct & 15;
         const int ty = ct >> 4;
         const int r0 = ty * R1;  // first tile row of this thread
@@ -669,7 +687,7 @@ __global__ void __launch_bounds__(Cfg<H, R1, T1, YW>::NTHREADS, 1)
 template <int H, int R1, int T1, int SU, int SA, int YW>
 size_t smem_bytes() {
     using C = Cfg<H, R1, T1, YW>;
-    constexpr int SS = YW > 0 ? 2 * YW : 1;
+    constexpr int SS = YW > 0 ? (SWB_PENCIL_SS > 0 ? SWB_PENCIL_SS : 2 * YW) : 1;
     return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
            (YW > 0 ? static_cast<size_t>(SS) * C::ATILE : 0) + 16 * (SU + SA + SS) + 4 * SA;
 }
@@ -830,8 +848,9 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // chunks fill 144 of 148 SMs instead of 132 (+2.4 %); at 512^3 it keeps 22 (20 rows: -8 %).
     // Ties go to the height that wastes fewer interior rows.  SWB_TPLAN=rows: row efficiency only
     // (the previous rule, development A/B).  A variant with a y-pencil warp streams a plane in
-    // kPencilTime of the time (SO 16, 20 rows: 219.4 against 208.5 GPts/s at 256^3; at 512^3 the
-    // 22-row tile without it stays ahead, 250 against 240).
+    // kPencilTime of the time (SO 16, 20 rows, pencil on the producer's sub-partition taking
+    // k >= 4: 230.5 against 209.5 GPts/s at 256^3 and 234.9 against 226.0 at 384^3; at 512^3 the
+    // 20-row pencil tile runs 252.3 against 250.0 for the 22-row tile without it).
     const int rows = g.y1 - g.y0;
     const int np_all = g.x1 - g.x0;
     const int zs_all = g.z0 & ~3;
@@ -852,7 +871,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         if (nchunk_out) *nchunk_out = best_nc;
         return best_cost * std::pow(static_cast<double>(t1), 0.25);
     };
-    constexpr double kPencilTime = 0.95;
+    constexpr double kPencilTime = 0.91;
     int t1_best = 0, yw_best = 0;
     double eff_best = -1.0, cost_best = 1e300;
     for (int yw : {0, 1})

@@ -1,5 +1,5 @@
 """K1 with the y-pencil warp (the SO 16 20-row variant: one warp computes the far y terms
-k >= 5 of every output plane into a shared-memory ring, k_tma.cu ypencil_loop), forced with
+k >= 4 of every output plane into a shared-memory ring, k_tma.cu ypencil_loop), forced with
 SWB_YW=1 / SWB_T1=20 on every configuration the plain K1 is tested on: random problems against
 the C restatement of the reference (<= 1e-5), fused z-slab exchange bitwise equal to one domain,
 10k steps within 1e-5, and the plan's choice (pencil at 256^3 SO 16, the 22-row tile without it
