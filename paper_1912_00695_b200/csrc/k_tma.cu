@@ -834,6 +834,20 @@ bool encode(CUtensorMap* map, const float* base, int n2, int n1, int nl0, int P2
 
 // Kernel plan for one handle: the variant (tile height by row efficiency), the column tiles and
 // the dim-0 chunk count.
+// First dim-2 column of z tile 0.  For H < 8, tiles start on a 64-float (256-byte) boundary when
+// that needs no extra tile, so the aux-tile rows (u[t-1], B, A: T1 x 64 floats) and the output rows
+// each sit in one 256-byte L2 segment instead of straddling two (the lanes left of z0 are masked
+// like the right edge); otherwise at z0 rounded down to a float4, which aligns the u box
+// (zt - A = z0 - H) instead.  Measured (profiles/zalign_r02.txt, 256^3): SO 8 307 -> 314 GPts/s
+// (512^3: 360 -> 373), SO 12 +0.4 %, SO 16 -0.4 % (its u box of 64 + 16 floats then spans three
+// segments), SO 4 unchanged (z0 & ~3 is already 0).  SWB_ZALIGN=0/1 forces either (development A/B).
+int tile_z_start(const Geo& g, int H) {
+    const int z4 = g.z0 & ~3, z64 = g.z0 & ~(kT2 - 1);
+    const char* env = std::getenv("SWB_ZALIGN");
+    const bool align = env ? env[0] == '1' : H < 8;
+    return align && ceil_div(g.z1 - z64, kT2) == ceil_div(g.z1 - z4, kT2) ? z64 : z4;
+}
+
 TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     TmaPlan p{};
     p.ok = 0;
@@ -853,7 +867,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // 20-row pencil tile runs 252.3 against 250.0 for the 22-row tile without it).
     const int rows = g.y1 - g.y0;
     const int np_all = g.x1 - g.x0;
-    const int zs_all = g.z0 & ~3;
+    const int zs_all = tile_z_start(g, H);
     const int tz_all = ceil_div(g.z1 - zs_all, kT2);
     const bool rows_only = std::getenv("SWB_TPLAN") && std::strcmp(std::getenv("SWB_TPLAN"), "rows") == 0;
     auto makespan = [&](int t1, int* nchunk_out) {
@@ -898,7 +912,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     p.A = (H + 3) / 4 * 4;
     p.threads = v->threads;
     p.smem_bytes = static_cast<int>(v->smem);
-    const int zs = g.z0 & ~3;
+    const int zs = tile_z_start(g, H);
     p.zs = zs;
     p.tiles_y = ceil_div(g.y1 - g.y0, p.T1);
     p.tiles_z = ceil_div(g.z1 - zs, kT2);
