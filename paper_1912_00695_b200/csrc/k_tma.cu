@@ -570,7 +570,13 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                         aflag[st] = need_damp;  // published by the arrive below (release)
                         mbar_expect_tx(full_a + 8 * st, (need_damp ? 3 : 2) * C::ATILE);
                         const unsigned dst = aring_s + st * 3 * C::ATILE;
-                        tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * st, pol_first);
+                        // u[t-1] evict_first, except at SO 16, whose tile rows straddle two 256-byte
+                        // L2 segments (tile_z_start): the neighbouring tile's half then survives
+                        // (+0.4 % at SO 16, -0.7 % at SO 8; profiles/um1_policy_r02.txt)
+                        if constexpr (H >= 8)
+                            tma_load3(dst, ma, zt, yt, p, full_a + 8 * st);
+                        else
+                            tma_load3_hint(dst, ma, zt, yt, p, full_a + 8 * st, pol_first);
                         // B (1/(m+g)) is re-read every step: default L2 policy (evict_first measured
                         // -3 % at 512^3 SO 8); u[t-1] and A stay evict_first
                         tma_load3(dst + C::ATILE, &maps.m, zt, yt, p, full_a + 8 * st);
