@@ -43,12 +43,16 @@ op.close()
 raw = np.array(buf[:], dtype=np.float64).reshape(2, 1024, 8)[0, :g]
 sm = raw[:, 5].astype(int)
 st = (raw[:, 3] - raw[:, 1]) / 1e3
+NCOL, NZT = int(os.environ.get("TRACE_NCOL", "36")), int(os.environ.get("TRACE_NZT", "4"))
 if os.environ.get("TRACE_DETAIL"):
     order = np.argsort(st)
     print("  fastest 6 (cta, sm, us):", [(int(b), int(sm[b]), round(float(st[b]), 2)) for b in order[:6]])
     print("  slowest 6 (cta, sm, us):", [(int(b), int(sm[b]), round(float(st[b]), 2)) for b in order[-6:]])
     for name, key in (("sm // 2 (TPC) parity", lambda b: (sm[b] // 2) % 2), ("sm < 74", lambda b: int(sm[b] < 74)),
-                      ("sm % 4", lambda b: sm[b] % 4)):
+                      ("sm % 4", lambda b: sm[b] % 4),
+                      # items = CTAs here (one item each): item = chunk * ncol + col, col = ytile * nzt + ztile
+                      ("chunk", lambda b: b // NCOL), ("z tile", lambda b: (b % NCOL) % NZT),
+                      ("y tile", lambda b: (b % NCOL) // NZT)):
         grp = {}
         for b in range(g):
             grp.setdefault(key(b), []).append(st[b])
