@@ -200,6 +200,47 @@ cudaError_t launch_inject(float* un, const long long* idx, const double* w, int 
     return cudaGetLastError();
 }
 
+// Receiver samples of up to three consecutive steps in one launch: the three u levels hold the
+// outputs of the last three steps, so the per-step sampler launch (2-3 us at small grids, where
+// the stencil step itself is ~6 us) is needed only every third step.  Row b of `out` (n floats)
+// is sampled from lev[b]; the arithmetic per sample is k_samplers'.
+struct SampleLevels {
+    const float* lev[3];
+};
+__global__ void k_samplers_batch(const SampleLevels L, int nb, const long long* __restrict__ idx,
+                                 const double* __restrict__ w, int n, float* __restrict__ out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n * nb) {
+        const int b = t / n, r = t - b * n;
+        const float* un = b == 0 ? L.lev[0] : (b == 1 ? L.lev[1] : L.lev[2]);
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const long long j = idx[8 * r + c];
+            if (j >= 0) v = __dadd_rn(v, __dmul_rn(w[8 * r + c], static_cast<double>(un[j])));
+        }
+        out[t] = static_cast<float>(v);
+    }
+}
+
+cudaError_t launch_samplers_batch(const float* const* lev, int nb, const long long* idx, const double* w, int n,
+                                  float* out, cudaStream_t s) {
+    if (n <= 0 || nb <= 0) return cudaSuccess;
+    SampleLevels L{{lev[0], nb > 1 ? lev[1] : lev[0], nb > 2 ? lev[2] : lev[0]}};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ceil_div(n * nb, 128));
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_samplers_batch, L, nb, idx, w, n, out);
+}
+
 cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
                             cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

@@ -64,6 +64,8 @@ cudaError_t launch_receivers(const float* un, const long long* idx, int n, float
                              cudaStream_t s);
 cudaError_t launch_samplers(const float* un, const long long* idx, const double* w, int n, float* out,
                             cudaStream_t s);
+cudaError_t launch_samplers_batch(const float* const* lev, int nb, const long long* idx, const double* w, int n,
+                                  float* out, cudaStream_t s);
 // Adjoint receiver injection: un[idx] += w * data[r] (8 corners per receiver, one rounding of the
 // double sum per corner, CAS loop so coinciding corners accumulate).
 cudaError_t launch_inject(float* un, const long long* idx, const double* w, int n, const float* data,

@@ -324,6 +324,7 @@ bool linked(const swb_handle* h) { return h->lo_remote || h->hi_remote || h->pee
 
 int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
     const int kmask = (h->lo_remote && !h->fused_lo ? 1 : 0) | (h->hi_remote && !h->fused_hi ? 2 : 0);
+    int rec_pending = 0;  // steps since the last receiver sampling launch
     for (int i = 0; i < nt;) {
         const int s = step0 + i;
         if (kmask) {  // kernel-based ordering for sides without fused support
@@ -360,11 +361,18 @@ int enqueue_steps(swb_handle* h, int step0, int nt, int slot0 = 0) {
             SWB_CUDA(launch_simple(h->H, form, h->geo, h->K, c, h->peer, h->stream));
         }
         ++h->launches;
-        if (!h->rec_owned.empty()) {
+        if (!h->rec_owned.empty() && (++rec_pending == 3 || i == nt - 1)) {
+            // receiver samples of the last rec_pending steps (step s' left its output in level
+            // (s' + 1) % 3, which steps s' + 1 and s' + 2 do not write): one launch per three steps
             const int owned = static_cast<int>(h->rec_owned.size());
-            SWB_CUDA(launch_samplers(h->u + ((s + 1) % 3) * h->level_floats, h->d_rec_idx, h->d_rec_w, owned,
-                                     h->d_traces + static_cast<long long>(slot0 + i) * owned, h->stream));
+            const int j0 = i + 1 - rec_pending;
+            const float* lev[3];
+            for (int b = 0; b < rec_pending; ++b)
+                lev[b] = h->u + ((step0 + j0 + b + 1) % 3) * h->level_floats;
+            SWB_CUDA(launch_samplers_batch(lev, rec_pending, h->d_rec_idx, h->d_rec_w, owned,
+                                           h->d_traces + static_cast<long long>(slot0 + j0) * owned, h->stream));
             ++h->launches;
+            rec_pending = 0;
         }
         if (kmask) {
             SWB_CUDA(launch_signal_flags(kmask & 1 ? h->lo_remote : nullptr, kmask & 2 ? h->hi_remote : nullptr,
