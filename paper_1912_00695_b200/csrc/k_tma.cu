@@ -931,15 +931,18 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // boundary read the shared planes at the same time (L2 hits), and neighbouring columns
     // stream the same planes concurrently (halo re-reads hit L2).  The chunk count minimises
     // the estimated makespan: rounds of items over the persistent CTAs x (chunk length +
-    // warm-up of 2H planes, which cost about half an output plane each).
+    // warm-up of 2H planes, which cost about half an output plane each).  Among equal makespans
+    // with items of at most 4 planes (small grids: each item is a short latency-bound pipeline
+    // fill) the most items win: more CTAs start at once and the average item is shorter
+    // (64^3 SO 2: 31 chunks 5.9 us per step, 49 chunks 5.4 us; scripts/small_sweep.py).
     int best = 1;
     double best_cost = 1e300;
-    for (int nc = 1; nc <= 32 && nc <= np; ++nc) {
+    for (int nc = 1; nc <= 64 && nc <= np; ++nc) {
         const long long items = static_cast<long long>(p.columns) * nc;
         const long long rounds = (items + num_sms - 1) / num_sms;
         const double len = static_cast<double>(np) / nc;
         const double cost = static_cast<double>(rounds) * (std::ceil(len) + 0.5 * 2 * H);
-        if (cost < best_cost - 1e-9) {
+        if (cost < best_cost - 1e-9 || (cost <= best_cost + 1e-9 && std::ceil(len) <= 4)) {
             best_cost = cost;
             best = nc;
         }
