@@ -820,8 +820,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+// L2 promotion of a map (SWB_PROMO_U / SWB_PROMO_A = 0, 64, 128 or 256 override it, development A/B).
+// 256 B, except the u boxes at SO <= 12: with the 256-byte aligned z tiles their 64 + 2A float rows
+// reach A floats into each neighbouring segment, and 128 B promotion fetched less of those
+// (512^3 SO 8: 374 -> 377 GPts/s; 256^3 within noise; profiles/promo_r02.txt).
+CUtensorMapL2promotion promo_env(const char* name, int dflt = 256) {
+    const char* env = std::getenv(name);
+    const int v = env ? std::atoi(env) : dflt;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 bool encode(CUtensorMap* map, const float* base, int n2, int n1, int nl0, int P2, int box0,
-            int box1) {
+            int box1, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     auto fn = get_encode();
     if (!fn) return false;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(n2), static_cast<cuuint64_t>(n1),
@@ -832,7 +844,7 @@ bool encode(CUtensorMap* map, const float* base, int n2, int n1, int nl0, int P2
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -967,13 +979,13 @@ cudaError_t tma_make_maps(const TmaPlan& plan, const Geo& g, int nl0, void* out)
     std::memset(maps, 0, sizeof(Maps));
     const int W2 = kT2 + 2 * plan.A;
     for (int l = 0; l < 3; ++l) {
-        if (!encode(&maps->u[l], g.lev[l], g.n2, g.n1, nl0, g.P2, W2, plan.T1 + 2 * plan.H))
+        if (!encode(&maps->u[l], g.lev[l], g.n2, g.n1, nl0, g.P2, W2, plan.T1 + 2 * plan.H, promo_env("SWB_PROMO_U", plan.H < 8 ? 128 : 256)))
             return cudaErrorInvalidValue;
-        if (!encode(&maps->a[l], g.lev[l], g.n2, g.n1, nl0, g.P2, kT2, plan.T1))
+        if (!encode(&maps->a[l], g.lev[l], g.n2, g.n1, nl0, g.P2, kT2, plan.T1, promo_env("SWB_PROMO_A")))
             return cudaErrorInvalidValue;
     }
-    if (!encode(&maps->m, g.m, g.n2, g.n1, nl0, g.P2, kT2, plan.T1)) return cudaErrorInvalidValue;
-    if (!encode(&maps->damp, g.damp, g.n2, g.n1, nl0, g.P2, kT2, plan.T1))
+    if (!encode(&maps->m, g.m, g.n2, g.n1, nl0, g.P2, kT2, plan.T1, promo_env("SWB_PROMO_A"))) return cudaErrorInvalidValue;
+    if (!encode(&maps->damp, g.damp, g.n2, g.n1, nl0, g.P2, kT2, plan.T1, promo_env("SWB_PROMO_A")))
         return cudaErrorInvalidValue;
     return cudaSuccess;
 }
