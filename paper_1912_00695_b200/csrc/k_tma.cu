@@ -156,6 +156,16 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
 #ifndef SWB_PENCIL_SS
 #define SWB_PENCIL_SS 0  // development override of the P_y ring depth (0: 2 per pencil warp)
 #endif
+#ifndef SWB_PY_AUX
+#define SWB_PY_AUX 1  // P_y in a fourth slot of the aux ring stage (one barrier pair for aux + P_y)
+#endif
+// With SWB_PY_AUX the pencil writes P_y of output plane p into the aux-ring stage of p and arrives on
+// its full barrier (initialised for the TMA producer's arrive plus the 32 pencil lanes), so the
+// consumers wait once and release once per plane for u[t-1], B, A and P_y together.
+template <int YW>
+constexpr bool py_aux() { return YW > 0 && SWB_PY_AUX != 0; }
+template <int YW>
+constexpr int aux_slots() { return py_aux<YW>() ? 4 : 3; }
 template <int H>
 constexpr int pencil_k() { return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : H - 4; }
 
@@ -168,7 +178,7 @@ struct YRing {
 // Pencil warp yw (of YW) takes output planes g = yw, yw + YW, ... of this CTA in the consumers'
 // order.  The consumers wait for P_y of output plane p before they release p's u-ring stage, so
 // the pencil's reads of that stage are ordered before the TMA overwrite (mbarrier release/acquire).
-template <int H, int T1, int SU, int SS, int YW>
+template <int H, int T1, int SU, int SS, int YW, int STAGE_F>
 __device__ __forceinline__ void ypencil_loop(int yw, int lane, const unsigned char* uring, float* sring,
                                              unsigned full_u, unsigned full_s, unsigned empty_s,
                                              const Coef& K, const Sched& sc, int first, int G, int nitems) {
@@ -194,7 +204,7 @@ __device__ __forceinline__ void ypencil_loop(int yw, int lane, const unsigned ch
             mbar_wait(empty_s + 8 * sst, sph ^ 1u);
             mbar_wait(full_u + 8 * ust, uph);
             const float* pl = ub + ust * (C::UPLANE / 4);
-            float* so = sb + sst * (T1 * kT2);
+            float* so = sb + sst * STAGE_F;
             // all NL rows first (no queue here: registers to spare), then k outer / outputs inner,
             // so SEG independent FFMA2 chains advance together
             float4 v[NL];
@@ -335,7 +345,7 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
         acc[i][0] = fma2(c1, dl, al);
         acc[i][1] = fma2(c1, dh, ah);
     }
-    if constexpr (YW > 0) {  // + P_y of this output plane (pencil warp)
+    if constexpr (YW > 0 && !py_aux<YW>()) {  // + P_y of this output plane (pencil warp)
         static_assert(R1 == 1, "pencil variants run one row per consumer thread");
         mbar_wait(yr.full + 8 * yr.st, yr.ph);
         const float4 sy = *reinterpret_cast<const float4*>(yr.col + yr.st * (T1 * kT2));
@@ -346,8 +356,14 @@ __device__ __forceinline__ void consumer_step(float4 (&Q)[R1][QN], int j, Item& 
     }
     // ---- aux tiles: u[t-1], m, damp ----
     mbar_wait(full_a + 8 * sa, pa_);
-    const float* aux = acol + sa * (3 * C::ATILE / 4);
+    const float* aux = acol + sa * (aux_slots<YW>() * C::ATILE / 4);
     const bool has_damp = aflag[sa] != 0u;
+    if constexpr (py_aux<YW>()) {  // + P_y of this output plane (pencil warp, fourth aux slot)
+        static_assert(R1 == 1, "pencil variants run one row per consumer thread");
+        const float4 sy = *reinterpret_cast<const float4*>(aux + 3 * C::ATILE / 4);
+        acc[0][0] = add2(acc[0][0], lo2(sy));
+        acc[0][1] = add2(acc[0][1], hi2(sy));
+    }
     float4 upv[R1], bv[R1], av[R1];
 #pragma unroll
     for (int i = 0; i < R1; ++i) {
@@ -463,9 +479,10 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* uring = smem;
     unsigned char* aring = smem + SU * C::UPLANE;
-    float* sring = reinterpret_cast<float*>(aring + SA * 3 * C::ATILE);  // YW > 0: P_y stages (T1 x 64)
+    constexpr int AS = aux_slots<YW>() * C::ATILE;  // bytes per aux stage
+    float* sring = reinterpret_cast<float*>(aring + SA * AS);  // YW > 0 without py_aux: P_y stages (T1 x 64)
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sring) +
-                                                 (YW > 0 ? SS * C::ATILE : 0));
+                                                 (YW > 0 && !py_aux<YW>() ? SS * C::ATILE : 0));
     unsigned* aflag = reinterpret_cast<unsigned*>(bars + 2 * (SU + SA + SS));  // damp-present per aux stage
     const unsigned full_u = smem_addr(bars), empty_u = full_u + 8 * SU;
     const unsigned full_a = empty_u + 8 * SU, empty_a = full_a + 8 * SA;
@@ -484,7 +501,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
             mbar_init(empty_u + 8 * i, 32 * C::NCW);  // every consumer thread arrives
         }
         for (int i = 0; i < SA; ++i) {
-            mbar_init(full_a + 8 * i, 1);
+            mbar_init(full_a + 8 * i, py_aux<YW>() ? 1 + 32 : 1);  // (+ the pencil lanes)
             mbar_init(empty_a + 8 * i, 32 * C::NCW);
         }
         for (int i = 0; i < SS; ++i) {
@@ -569,7 +586,7 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
                         const unsigned need_damp = (!dfl || dfl[p]) ? 1u : 0u;
                         aflag[st] = need_damp;  // published by the arrive below (release)
                         mbar_expect_tx(full_a + 8 * st, (need_damp ? 3 : 2) * C::ATILE);
-                        const unsigned dst = aring_s + st * 3 * C::ATILE;
+                        const unsigned dst = aring_s + st * AS;
                         // u[t-1] evict_first, except at SO 16, whose tile rows straddle two 256-byte
                         // L2 segments (tile_z_start): the neighbouring tile's half then survives
                         // (+0.4 % at SO 16, -0.7 % at SO 8; profiles/um1_policy_r02.txt)
@@ -591,7 +608,12 @@ __device__ __forceinline__ void tma_body(const Maps& maps, const Geo& g, const C
     } else if (is_pencil) {
         // ===== y-pencil warps =====
         if constexpr (YW > 0)
-            ypencil_loop<H, T1, SU, SS, YW>(warp - PW0, lane, uring, sring, full_u, full_s, empty_s, K,
+            if constexpr (py_aux<YW>())
+                ypencil_loop<H, T1, SU, SA, YW, AS / 4>(warp - PW0, lane, uring,
+                                                        reinterpret_cast<float*>(aring) + 3 * C::ATILE / 4, full_u,
+                                                        full_a, empty_a, K, sc, first, G, nitems);
+            else
+                ypencil_loop<H, T1, SU, SS, YW, T1 * kT2>(warp - PW0, lane, uring, sring, full_u, full_s, empty_s, K,
                                             sc, first, G, nitems);
     } else {
         // ===== consumers =====
@@ -694,8 +716,8 @@ template <int H, int R1, int T1, int SU, int SA, int YW>
 size_t smem_bytes() {
     using C = Cfg<H, R1, T1, YW>;
     constexpr int SS = YW > 0 ? (SWB_PENCIL_SS > 0 ? SWB_PENCIL_SS : 2 * YW) : 1;
-    return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * 3 * C::ATILE +
-           (YW > 0 ? static_cast<size_t>(SS) * C::ATILE : 0) + 16 * (SU + SA + SS) + 4 * SA;
+    return static_cast<size_t>(SU) * C::UPLANE + static_cast<size_t>(SA) * aux_slots<YW>() * C::ATILE +
+           (YW > 0 && !py_aux<YW>() ? static_cast<size_t>(SS) * C::ATILE : 0) + 16 * (SU + SA + SS) + 4 * SA;
 }
 
 // Variant table: (H, R1, T1, SU, SA) chosen per space order to fit 227 KB of smem.
@@ -881,8 +903,8 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // Ties go to the height that wastes fewer interior rows.  SWB_TPLAN=rows: row efficiency only
     // (the previous rule, development A/B).  A variant with a y-pencil warp streams a plane in
     // kPencilTime of the time (SO 16, 20 rows, pencil on the producer's sub-partition taking
-    // k >= 4: 230.5 against 209.5 GPts/s at 256^3 and 234.9 against 226.0 at 384^3; at 512^3 the
-    // 20-row pencil tile runs 252.3 against 250.0 for the 22-row tile without it).
+    // k >= 4, P_y in the aux ring: 235.8 against 209.5 GPts/s at 256^3; at 512^3 the 20-row pencil
+    // tile runs 258 against 250 for the 22-row tile without it; profiles/pyaux_r02.txt).
     const int rows = g.y1 - g.y0;
     const int np_all = g.x1 - g.x0;
     const int zs_all = tile_z_start(g, H);
@@ -903,7 +925,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         if (nchunk_out) *nchunk_out = best_nc;
         return best_cost * std::pow(static_cast<double>(t1), 0.25);
     };
-    constexpr double kPencilTime = 0.91;
+    constexpr double kPencilTime = 0.89;
     int t1_best = 0, yw_best = 0;
     double eff_best = -1.0, cost_best = 1e300;
     for (int yw : {0, 1})
