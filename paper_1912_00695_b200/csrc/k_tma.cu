@@ -166,8 +166,15 @@ template <int YW>
 constexpr bool py_aux() { return YW > 0 && SWB_PY_AUX != 0; }
 template <int YW>
 constexpr int aux_slots() { return py_aux<YW>() ? 4 : 3; }
+#ifndef SWB_PENCIL_K6
+#define SWB_PENCIL_K6 4  // split point of the SO 12 pencil variant (k >= 3 / 5 measured slower, pencil12_r02.txt)
+#endif
 template <int H>
-constexpr int pencil_k() { return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : H - 4; }
+constexpr int pencil_k() { return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : (H == 6 ? SWB_PENCIL_K6 : H - 4); }
+// A pencil lane holds SEG/NSUB + 2H rows at a time (the halo rows between sub-segments are read
+// twice): SO 12's 28-row tile has 14 rows per pencil, two sub-segments fit its 128-register cap.
+template <int H>
+constexpr int pencil_nsub() { return H == 6 ? 2 : 1; }
 
 struct YRing {
     unsigned full, empty;  // mbarriers of stage 0 (8 bytes apart)
@@ -186,6 +193,7 @@ __device__ __forceinline__ void ypencil_loop(int yw, int lane, const unsigned ch
     constexpr int SEG = T1 / 2;
     constexpr int NL = SEG + 2 * H;
     constexpr int KP = pencil_k<H>();
+    constexpr int SUB = (SEG + pencil_nsub<H>() - 1) / pencil_nsub<H>();
     static_assert(T1 % 2 == 0 && KP >= 2, "two pencils per column; k = 1 stays with the consumers");
     const int tz = lane & 15, seg = lane >> 4;
     const float* ub = reinterpret_cast<const float*>(uring) + seg * SEG * C::W2 + C::A + 4 * tz;
@@ -205,26 +213,35 @@ __device__ __forceinline__ void ypencil_loop(int yw, int lane, const unsigned ch
             mbar_wait(full_u + 8 * ust, uph);
             const float* pl = ub + ust * (C::UPLANE / 4);
             float* so = sb + sst * STAGE_F;
-            // all NL rows first (no queue here: registers to spare), then k outer / outputs inner,
-            // so SEG independent FFMA2 chains advance together
-            float4 v[NL];
+            // all rows of a sub-segment first (no queue here), then k outer / outputs inner, so the
+            // sub-segment's independent FFMA2 chains advance together
 #pragma unroll
-            for (int i = 0; i < NL; ++i) v[i] = *reinterpret_cast<const float4*>(pl + i * C::W2);
-            float2 al[SEG], ah[SEG];
+            for (int s0 = 0; s0 < SEG; s0 += SUB) {
+                constexpr int NV = SUB + 2 * H;
+                float4 v[NV];
 #pragma unroll
-            for (int o = 0; o < SEG; ++o) al[o] = ah[o] = splat(0.f);
+                for (int i = 0; i < NV; ++i)
+                    if (s0 + i < NL) v[i] = *reinterpret_cast<const float4*>(pl + (s0 + i) * C::W2);
+                float2 al[SUB], ah[SUB];
 #pragma unroll
-            for (int k = H; k >= KP; --k) {
-                const float2 ck = splat(K.c[k]);
+                for (int o = 0; o < SUB; ++o) al[o] = ah[o] = splat(0.f);
 #pragma unroll
-                for (int o = 0; o < SEG; ++o) {  // output row o of the pencil: centre v[o + H]
-                    al[o] = fma2(ck, add2(lo2(v[o + H - k]), lo2(v[o + H + k])), al[o]);
-                    ah[o] = fma2(ck, add2(hi2(v[o + H - k]), hi2(v[o + H + k])), ah[o]);
+                for (int k = H; k >= KP; --k) {
+                    const float2 ck = splat(K.c[k]);
+#pragma unroll
+                    for (int o = 0; o < SUB; ++o) {  // output row s0 + o of the pencil: centre v[o + H]
+                        if (s0 + o < SEG) {
+                            al[o] = fma2(ck, add2(lo2(v[o + H - k]), lo2(v[o + H + k])), al[o]);
+                            ah[o] = fma2(ck, add2(hi2(v[o + H - k]), hi2(v[o + H + k])), ah[o]);
+                        }
+                    }
                 }
-            }
 #pragma unroll
-            for (int o = 0; o < SEG; ++o)
-                *reinterpret_cast<float4*>(so + o * kT2) = make_float4(al[o].x, al[o].y, ah[o].x, ah[o].y);
+                for (int o = 0; o < SUB; ++o)
+                    if (s0 + o < SEG)
+                        *reinterpret_cast<float4*>(so + (s0 + o) * kT2) =
+                            make_float4(al[o].x, al[o].y, ah[o].x, ah[o].y);
+            }
             mbar_arrive(full_s + 8 * sst);  // release: this lane's P_y stores
         }
         gseq += np;
@@ -739,7 +756,8 @@ size_t smem_bytes() {
     X(5, 1, 28, 10, 4, 2, 0)        \
     X(6, 1, 28, 10, 3, 4, 0)        \
     X(8, 1, 20, 11, 3, 4, 0)        \
-    X(8, 1, 20, 13, 3, 6, 1)
+    X(8, 1, 20, 13, 3, 6, 1)        \
+    X(6, 1, 28, 10, 3, 2, 1)
 
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
@@ -926,6 +944,10 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         return best_cost * std::pow(static_cast<double>(t1), 0.25);
     };
     constexpr double kPencilTime = 0.89;
+    // SO 12: the 28-row tile with a pencil warp (16 warps at 128 registers, queue unroll 2, P_y
+    // through the aux ring) against the 15-warp tile without it: 260.8 against 250.8 GPts/s at 256^3,
+    // 276.7 / 267.0 at 384^3, 310.0 / 304.7 at 512^3 (profiles/pencil12_aux_r02.txt)
+    constexpr double kPencilTime12 = 0.96;
     int t1_best = 0, yw_best = 0;
     double eff_best = -1.0, cost_best = 1e300;
     for (int yw : {0, 1})
@@ -935,7 +957,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
             const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
             const double cost = rows_only || np_all <= 0 || rows <= 0
                                     ? 0.0
-                                    : makespan(cand, nullptr) * (yw ? kPencilTime : 1.0);
+                                    : makespan(cand, nullptr) * (yw ? (H == 8 ? kPencilTime : kPencilTime12) : 1.0);
             if (cost < cost_best * (1 - 1e-9) || (cost <= cost_best * (1 + 1e-9) && eff > eff_best + 1e-9)) {
                 cost_best = cost;
                 eff_best = eff;

@@ -136,10 +136,42 @@ def test_pencil_10k_steps_128(force_pencil):
     assert rel_l2(fast.get_level(nt % 3), exact.get_level(nt % 3)) <= 1e-5
 
 
-@pytest.mark.parametrize("n,expect", [(256, (1, 20)), (512, (1, 20)), (320, (0, 22))])
-def test_plan_picks_pencil_where_faster(n, expect):
-    prob = P.make_wave_problem(P.WaveProblemConfig(shape=(n,) * 3, spacing=(10., 10., 10.), space_order=16,
+@pytest.mark.parametrize("n,so,expect", [(256, 16, (1, 20)), (512, 16, (1, 20)), (320, 16, (0, 22)),
+                                           (256, 12, (1, 28)), (512, 12, (1, 28))])
+def test_plan_picks_pencil_where_faster(n, so, expect):
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=(n,) * 3, spacing=(10., 10., 10.), space_order=so,
                                                    steps=1))
     op = P.Operator(prob)
     assert pencil_variant(op) == expect
     op.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pencil_so12_random_configuration(seed, monkeypatch):
+    """The SO 12 pencil variant (28-row tile, pencil rows in two sub-segments, P_y through the aux
+    ring) forced on random damped heterogeneous problems against the C restatement (<= 1e-5)."""
+    monkeypatch.setenv("SWB_YW", "1")
+    monkeypatch.setenv("SWB_T1", "28")
+    rng = np.random.default_rng(6100 + seed)
+    so, h = 12, 6
+    shape = tuple(int(rng.integers(2 * h + 3, 2 * h + 60)) for _ in range(3))
+    nt = int(rng.integers(3, 25))
+    vel = (1500 + 1500 * rng.random(shape)).astype(np.float32)
+    damp = float(rng.choice([0.0, 0.02, 0.1]))
+    width = int(rng.integers(1, 6))
+    src = [int(rng.integers(h, s - h)) for s in shape]
+    rec = np.array([[int(rng.integers(0, s)) for s in shape] for _ in range(6)], np.int32)
+    init = [(rng.standard_normal(shape) * 1e-2).astype(np.float32) for _ in range(3)]
+    prob = P.make_wave_problem(P.WaveProblemConfig(shape=shape, spacing=(10.0, 10.0, 10.0), space_order=so,
+                                                   steps=nt, velocity_field=vel, damp_max=damp,
+                                                   damp_width=width, source_point=src))
+    ref = O.port_run(O.OracleConfig(shape=shape, space_order=so, steps=nt, velocity_field=vel, damp_max=damp,
+                                    damp_width=width, source_point=src), initial_u=init, receivers=rec)
+    op = P.Operator(prob, receivers=rec)
+    assert pencil_variant(op) == (1, 28)
+    for lvl in range(3):
+        op.set_level(lvl, init[lvl])
+    r = op.apply(nt, 0)
+    fl = nt % 3
+    assert rel_l2(op.get_level(fl), ref["levels"][fl]) <= 1e-5
+    assert rel_l2(r.rec_traces, ref["rec_traces"]) <= 1e-5
