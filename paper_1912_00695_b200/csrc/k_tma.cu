@@ -169,12 +169,17 @@ constexpr int aux_slots() { return py_aux<YW>() ? 4 : 3; }
 #ifndef SWB_PENCIL_K6
 #define SWB_PENCIL_K6 4  // split point of the SO 12 pencil variant (k >= 3 / 5 measured slower, pencil12_r02.txt)
 #endif
+#ifndef SWB_PENCIL_K4
+#define SWB_PENCIL_K4 2  // split point of the SO 8 pencil variant (k >= 3: -0.5 %, k >= 4: -1.6 % at 256^3)
+#endif
 template <int H>
-constexpr int pencil_k() { return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : (H == 6 ? SWB_PENCIL_K6 : H - 4); }
+constexpr int pencil_k() {
+    return SWB_PENCIL_K > 0 ? SWB_PENCIL_K : (H == 6 ? SWB_PENCIL_K6 : (H == 4 ? SWB_PENCIL_K4 : H - 4));
+}
 // A pencil lane holds SEG/NSUB + 2H rows at a time (the halo rows between sub-segments are read
 // twice): SO 12's 28-row tile has 14 rows per pencil, two sub-segments fit its 128-register cap.
 template <int H>
-constexpr int pencil_nsub() { return H == 6 ? 2 : 1; }
+constexpr int pencil_nsub() { return H <= 6 ? 2 : 1; }
 
 struct YRing {
     unsigned full, empty;  // mbarriers of stage 0 (8 bytes apart)
@@ -757,7 +762,8 @@ size_t smem_bytes() {
     X(6, 1, 28, 10, 3, 4, 0)        \
     X(8, 1, 20, 11, 3, 4, 0)        \
     X(8, 1, 20, 13, 3, 6, 1)        \
-    X(6, 1, 28, 10, 3, 2, 1)
+    X(6, 1, 28, 10, 3, 2, 1)        \
+    X(4, 1, 28, 8, 4, 4, 1)
 
 
 using KernelFn = void (*)(Maps, Geo, Coef, Ctl, Peer, Sched);
@@ -948,6 +954,9 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // through the aux ring) against the 15-warp tile without it: 260.8 against 250.8 GPts/s at 256^3,
     // 276.7 / 267.0 at 384^3, 310.0 / 304.7 at 512^3 (profiles/pencil12_aux_r02.txt)
     constexpr double kPencilTime12 = 0.96;
+    // SO 8: the same with k >= 2 in the pencil: 318.0 against 313.4 GPts/s at 256^3, equal at 512^3
+    // (profiles/pencil8_r02.txt)
+    constexpr double kPencilTime8 = 0.985;
     int t1_best = 0, yw_best = 0;
     double eff_best = -1.0, cost_best = 1e300;
     for (int yw : {0, 1})
@@ -957,7 +966,7 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
             const double eff = static_cast<double>(rows) / (static_cast<double>(ceil_div(rows, cand)) * cand);
             const double cost = rows_only || np_all <= 0 || rows <= 0
                                     ? 0.0
-                                    : makespan(cand, nullptr) * (yw ? (H == 8 ? kPencilTime : kPencilTime12) : 1.0);
+                                    : makespan(cand, nullptr) * (yw ? (H == 8 ? kPencilTime : H == 6 ? kPencilTime12 : kPencilTime8) : 1.0);
             if (cost < cost_best * (1 - 1e-9) || (cost <= cost_best * (1 + 1e-9) && eff > eff_best + 1e-9)) {
                 cost_best = cost;
                 eff_best = eff;

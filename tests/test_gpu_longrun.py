@@ -42,3 +42,13 @@ def test_10k_steps_128(so, medium):
     err = rel(fast.get_level(fl), exact.get_level(fl))
     assert err <= TOL, err
     assert rel(rf.rec_traces, re.rec_traces) <= TOL
+
+
+@pytest.mark.parametrize("so,t1,medium", [(8, 28, "constant"), (8, 28, "hetero-damped"), (12, 28, "constant"),
+                                          (12, 28, "hetero-damped"), (16, 20, "constant")])
+def test_10k_steps_128_pencil_variants(so, t1, medium, monkeypatch):
+    """The y-pencil variants (far y terms summed by the pencil warp, a different summation order)
+    forced at 128^3, where the plan takes the tile without the pencil at SO 8/12."""
+    monkeypatch.setenv("SWB_YW", "1")
+    monkeypatch.setenv("SWB_T1", str(t1))
+    test_10k_steps_128(so, medium)
