@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2f evidence (final kernel: SO 16 P_y in the aux ring, pencil tile also at 512^3): ncu --set full of
+# Round-2f/2g evidence (r02g: final kernel with pencil variants at SO 8/12/16, P_y in the aux ring): ncu --set full of
 # K1 at SO 4-16 + the bench launch list (profile_box.sh), steady-state DRAM of every 256^3 / 512^3 case.
 TAG=${TAG:-r02f}
 bash scripts/profile_box.sh $TAG
