@@ -761,7 +761,7 @@ size_t smem_bytes() {
     X(5, 1, 28, 10, 4, 2, 0)        \
     X(6, 1, 28, 10, 3, 4, 0)        \
     X(8, 1, 20, 11, 3, 4, 0)        \
-    X(8, 1, 20, 13, 3, 6, 1)        \
+    X(8, 1, 20, 13, 3, 3, 1)        \
     X(6, 1, 28, 10, 3, 2, 1)        \
     X(4, 1, 28, 8, 4, 4, 1)
 
@@ -792,7 +792,9 @@ int preferred_unr(int H) {
     const char* env = std::getenv("SWB_UNR");
     if (env && env[0] >= '1' && env[0] <= '9') return env[0] - '0';
     // measured on B200 at 256^3 and 512^3: 4 for SO 8, 12 and 16, 2 for SO 10/14;
-    // the SO 16 pencil variant exists only with 6 (+0.4 % over 4) and is found by the fallback
+    // the SO 16 pencil variant exists only with 3 and is found by the fallback (with P_y through the
+    // aux ring, 256^3 / 384^3 / 512^3 GPts/s: UNR 2 233 / 238 / 255, 3 239 / 245 / 261, 4 239 / 243 / 261,
+    // 5 239 / 245 / 261, 6 236 / 241 / 258, 8 222 / 228 / 244; profiles/pencil16_unr_r02.txt)
     // (SO 8 runs the rotating queue, which ignores UNR)
     return H == 4 || H == 6 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
 }
