@@ -762,7 +762,7 @@ size_t smem_bytes() {
     X(6, 1, 28, 10, 3, 4, 0)        \
     X(8, 1, 20, 11, 3, 4, 0)        \
     X(8, 1, 20, 13, 3, 3, 1)        \
-    X(6, 1, 28, 10, 3, 2, 1)        \
+    X(6, 1, 28, 10, 3, 3, 1)        \
     X(4, 1, 28, 8, 4, 4, 1)
 
 
@@ -794,7 +794,8 @@ int preferred_unr(int H) {
     // measured on B200 at 256^3 and 512^3: 4 for SO 8, 12 and 16, 2 for SO 10/14;
     // the SO 16 pencil variant exists only with 3 and is found by the fallback (with P_y through the
     // aux ring, 256^3 / 384^3 / 512^3 GPts/s: UNR 2 233 / 238 / 255, 3 239 / 245 / 261, 4 239 / 243 / 261,
-    // 5 239 / 245 / 261, 6 236 / 241 / 258, 8 222 / 228 / 244; profiles/pencil16_unr_r02.txt)
+    // 5 239 / 245 / 261, 6 236 / 241 / 258, 8 222 / 228 / 244; profiles/pencil16_unr_r02.txt); the SO 12
+    // pencil variant likewise only with 3 (UNR 1 / 2 / 3 at 256^3: 250 / 261 / 266 GPts/s, pencil12_unr_r02.txt)
     // (SO 8 runs the rotating queue, which ignores UNR)
     return H == 4 || H == 6 || H == 8 ? 4 : (H >= 5 ? 2 : 1);
 }
@@ -952,10 +953,10 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
         return best_cost * std::pow(static_cast<double>(t1), 0.25);
     };
     constexpr double kPencilTime = 0.89;
-    // SO 12: the 28-row tile with a pencil warp (16 warps at 128 registers, queue unroll 2, P_y
-    // through the aux ring) against the 15-warp tile without it: 260.8 against 250.8 GPts/s at 256^3,
-    // 276.7 / 267.0 at 384^3, 310.0 / 304.7 at 512^3 (profiles/pencil12_aux_r02.txt)
-    constexpr double kPencilTime12 = 0.96;
+    // SO 12: the 28-row tile with a pencil warp (16 warps at 128 registers, queue unroll 3, P_y
+    // through the aux ring) against the 15-warp tile without it: 266.0 against 250.8 GPts/s at 256^3,
+    // 282.3 / 267.0 at 384^3, 323.9 / 304.7 at 512^3 (profiles/pencil12_aux_r02.txt, pencil12_unr_r02.txt)
+    constexpr double kPencilTime12 = 0.94;
     // SO 8: the same with k >= 2 in the pencil: 318.0 against 313.4 GPts/s at 256^3, equal at 512^3
     // (profiles/pencil8_r02.txt)
     constexpr double kPencilTime8 = 0.985;
