@@ -930,8 +930,10 @@ TmaPlan tma_plan(int H, const Geo& g, int num_sms) {
     // Ties go to the height that wastes fewer interior rows.  SWB_TPLAN=rows: row efficiency only
     // (the previous rule, development A/B).  A variant with a y-pencil warp streams a plane in
     // kPencilTime of the time (SO 16, 20 rows, pencil on the producer's sub-partition taking
-    // k >= 4, P_y in the aux ring: 235.8 against 209.5 GPts/s at 256^3; at 512^3 the 20-row pencil
-    // tile runs 258 against 250 for the 22-row tile without it; profiles/pyaux_r02.txt).
+    // k >= 4, P_y in the aux ring, queue unroll 3: 239.4 against 209.5 GPts/s at 256^3; at 512^3 the
+    // 20-row pencil tile runs 261 against 250 for the 22-row tile without it; profiles/pyaux_r02.txt,
+    // pencil16_unr_r02.txt; the factor is kept at the 0.89 measured with unroll 6, which already
+    // puts 256^3, 384^3 and 512^3 on the pencil tile and 320^3 / 448^3 on the 22-row one).
     const int rows = g.y1 - g.y0;
     const int np_all = g.x1 - g.x0;
     const int zs_all = tile_z_start(g, H);
