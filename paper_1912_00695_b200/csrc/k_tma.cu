@@ -145,8 +145,13 @@ __device__ __forceinline__ void epilogue_store(const float4* out, int p, long lo
 // on B200 (256^3, 20-row tile, GPts/s; profiles/pencil_r02.txt, pencil_place_r02.txt):
 //   warp 11: kP = 3: 202, 4: 209, 5: 219, 6: 214, 7: 209, 8: 201;   no pencil 208.5 / 209.5
 //   warp 4:  kP = 3: 227.9, 4: 230.6, 5: 225.6
-// (SO 8 and SO 12 variants with a pencil warp, 16 warps at 128 registers, measured slower:
-// SO 8 k >= 3: 307 -> 302, k >= 2: 281; SO 12 k >= 4: 251 -> 247, k >= 5: 242 GPts/s at 256^3)
+// With P_y handed over through the aux ring (SWB_PY_AUX, below) the pencil costs the consumers no
+// barrier, and the SO 8 and SO 12 variants (28 rows + pencil = 16 warps at 128 registers) pay off too:
+// SO 8 k >= 2: 313 -> 318, SO 12 k >= 4: 251 -> 266 GPts/s at 256^3 (with their own ring they had
+// measured slower or equal: profiles/pencil_r02.txt, pencil12_r02.txt; now pencil8_r02.txt,
+// pencil12_aux_r02.txt, pencil12_unr_r02.txt).
+// Ring roles with SWB_PY_AUX: ypencil_loop's (sring, SS, full_s, empty_s, STAGE_F) are the aux ring's
+// fourth slot, SA stages, its full / empty barriers and its stage stride; without it, the P_y ring's.
 #ifndef SWB_PENCIL_K
 #define SWB_PENCIL_K 0  // development override of the pencil split point (0: H - 4)
 #endif
