@@ -3,8 +3,9 @@
 // One persistent CTA per SM strides over work items (column tile x dim-0 chunk): a column
 // tile is T1 rows (dim 1) x 64 cols (dim 2) of output points; the CTA streams it along dim 0
 // (the reference's slowest axis "x"; the north star's "z-slab" axis) over the chunk's planes.
-// Warp 0 is the TMA producer (lane 0: u ring, lane 1: aux ring); warps 1..NCW are consumers;
-// the SO 16 20-row variant adds one y-pencil warp (far y terms, see ypencil_loop).
+// Warp 0 is the TMA producer (lane 0: u ring, lane 1: aux ring); the pencil variants (SO 8 and 12 on
+// 28-row tiles, SO 16 on 20-row tiles) have a y-pencil warp at warp 4 (far y terms, see ypencil_loop);
+// the other warps are consumers.
 //
 //   u ring  : halo-padded planes of u[t] ((T1+2H) x (64+2A) floats) loaded by
 //             cp.async.bulk.tensor.3d; a plane stays resident from its arrival (when the
@@ -13,6 +14,7 @@
 //             H planes later.  Depth S_U = H + 1 + prefetch.
 //   aux ring: u[t-1], B, A tiles (T1 x 64) of the output plane, one TMA each (A only where
 //             the tile is damped); B and A are the coefficient fields that replace m and damp.
+//             Pencil variants add a fourth slot, P_y, written by the pencil warp.
 //   register queue: each consumer thread keeps u[t] of its R1 x 4 points for the 2H+1
 //             planes around the output plane (the dim-0 stencil never touches smem).
 //
